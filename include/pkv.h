@@ -1,0 +1,163 @@
+/*
+ * pkv.h -- C ABI of the B200-native PatternKV codec (libpkv_b200.so).
+ *
+ * The reference (patternkv, pure Python/numpy) has no FFI; its drop-in
+ * surface is the Python module API re-exported by pkg/src/patternkv/__init__.py:10-94.
+ * Each entry point below names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/patternkv/).  Plain C types
+ * only: device pointers are `void*`/typed pointers to CUDA global memory,
+ * streams are `cudaStream_t` passed as `void*`.
+ *
+ * Status codes follow the reference error taxonomy (errors.py:9-14):
+ *   PKV_OK 0, PKV_USAGE 1 (UsageError, CLI exit 1), PKV_DATA 2 (DataError,
+ *   CLI exit 2), PKV_CUDA 3 (device/runtime failure; no reference analogue).
+ * pkv_last_error() returns the thread-local message of the last failure and
+ * the element index it refers to (-1 if none).
+ *
+ * Ownership: the library owns every cache arena; callers own the buffers they
+ * pass.  One writer stream per cache (the reference's single-writer
+ * HeadCacheState); reads are stream ordered.  Units (batch x
+ * layer x kv-head) are independent and advance in lockstep (same token count).
+ */
+#ifndef PKV_H_
+#define PKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PKV_OK 0
+#define PKV_USAGE 1
+#define PKV_DATA 2
+#define PKV_CUDA 3
+
+/* element types of caller tensors */
+#define PKV_F16 1
+#define PKV_F32 2
+#define PKV_F64 3
+#define PKV_BF16 4
+
+/* cache flags */
+#define PKV_FLAG_DECISIONS 1 /* keep per-token gate ranges (GateDecision records) */
+#define PKV_FLAG_STATS 2     /* count fp64 refinements / exact-division fallbacks */
+
+/* EngineConfig, field for field (engine.py:38-83) */
+typedef struct pkv_config {
+  int32_t bits;              /* 2, 4 or 8 (quant.py:18 SUPPORTED_BITS) */
+  int32_t pattern_count;     /* |M| mined per side at prefill */
+  int32_t group_size;        /* G, K per-channel group length; <= 128 on the GPU */
+  int32_t residual_window;   /* W >= G, exact window */
+  double alpha;              /* gate level in (0, 0.5] */
+  int32_t use_k_patterns;
+  int32_t use_v_patterns;
+  int32_t generate_new_patterns;
+  int32_t use_v_gate;
+  int32_t use_k_gate;
+  int64_t seed;              /* K mining seed; V uses seed + 1 (engine.py:157-159) */
+} pkv_config;
+
+typedef struct pkv_cache pkv_cache;
+
+typedef struct pkv_cache_info {
+  int32_t n_units, head_dim, head_dim_padded, in_dtype;
+  int64_t token_count;      /* HeadCacheState.token_count (engine.py:116) */
+  int64_t committed_count;  /* engine.py:121-123 */
+  int32_t window_len;       /* len(window_k) */
+  int32_t window_slot0;     /* ring slot of the oldest window row */
+  int32_t n_blocks;         /* len(k_blocks) */
+  int32_t pattern_capacity;
+  int64_t token_capacity;
+  int32_t block_bytes;      /* packed bytes per K (or V) block, fragment layout */
+  uint32_t n_refined;       /* fp64 re-matches (PKV_FLAG_STATS) */
+  uint32_t n_exact_div;     /* exact-division quantizer fallbacks (PKV_FLAG_STATS) */
+} pkv_cache_info;
+
+int pkv_version(void);
+const char* pkv_last_error(int64_t* index);
+
+/* gate.py:23-71 z_quantile and gate.py:74-106 contraction_threshold (host) */
+int pkv_z_quantile(double alpha, double* out);
+int pkv_threshold(int32_t head_dim, double alpha, double* out);
+/* engine.py:62-75 EngineConfig.__post_init__ */
+int pkv_config_validate(const pkv_config* cfg);
+
+/* HeadCacheState(config, head_dim) x n_units (engine.py:104-119); max_tokens and
+ * max_patterns are initial capacities (the cache grows on demand). */
+int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t head_dim, int32_t in_dtype,
+                     int64_t max_tokens, int32_t max_patterns, int32_t flags, pkv_cache** out);
+int pkv_cache_destroy(pkv_cache* c);
+int pkv_cache_info_get(pkv_cache* c, pkv_cache_info* out);
+int pkv_cache_reserve(pkv_cache* c, int64_t max_tokens, int32_t max_patterns, void* stream);
+/* drop every committed/window token (token_count = 0) but keep the pattern
+ * tables when keep_patterns != 0, so the next pkv_prefill with NULL seed
+ * indices re-encodes against the same tables (re-prefill of a slot). */
+int pkv_cache_reset(pkv_cache* c, int32_t keep_patterns, void* stream);
+
+/* engine.py:132-139 / :180-181 finiteness checks: *first_bad = flat index of the
+ * first non-finite element or -1.  Synchronous on `stream`. */
+int pkv_check_finite(const void* x, int32_t dtype, int64_t n, int64_t* first_bad, void* stream);
+
+/* mine_patterns (patterns.py:145-158) for every unit of one side (0 = K, 1 = V).
+ * x: device [U][T][D] of the cache dtype; first_idx: host [U] = first seed index
+ * np.random.default_rng(seed).integers(T) (patterns.py:103,135).  history/niter
+ * (optional, host) receive the objective history [U][25] and its length [U]. */
+int pkv_mine(pkv_cache* c, int32_t side, const void* x, int64_t T, const int64_t* first_idx,
+             double* history, int32_t* niter, void* stream);
+/* install pattern tables (device [U][P][D] fp64) for one side */
+int pkv_set_patterns(pkv_cache* c, int32_t side, const double* pat, int32_t P, void* stream);
+
+/* prefill (engine.py:142-169): mine K (first_k) and V (first_v) unless the
+ * pointer is NULL (tables kept), commit T - min(T, W) tokens in spans of G,
+ * keep the newest min(T, W) rows as the exact window.  k, v: device [U][T][D]. */
+int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T, const int64_t* first_k,
+                const int64_t* first_v, void* stream);
+
+/* append_decode_token (engine.py:172-198) for all units: k, v device [U][D]. */
+int pkv_append(pkv_cache* c, const void* k, const void* v, void* stream);
+
+/* decode attention (new; semantics = softmax over committed_matrices +
+ * window, engine.py:296-303): q device fp32 [U][gqa][D], out device fp32
+ * [U][gqa][D]. */
+int pkv_decode_attn(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, float* out, void* stream);
+
+/* committed_matrices / reconstruct_token (engine.py:271-303), exact fp64:
+ * committed tokens [t0, t1) -> device [U][t1-t0][D] each. */
+int pkv_dequant(pkv_cache* c, int64_t t0, int64_t t1, double* k_out, double* v_out, void* stream);
+
+/* unpacked integer codes of committed tokens [t0, t1): device uint8 [U][n][D]
+ * (token-major) for K and V; pack with pkv_pack_codes for the reference bytes. */
+int pkv_export_codes(pkv_cache* c, int64_t t0, int64_t t1, uint8_t* k_codes, uint8_t* v_codes, void* stream);
+
+/* Raw device arena pointers of the cache (read-only views for export / PKVS
+ * snapshots): name in {"kpat64","vpat64","kparam64","vparam64","kidx","vidx",
+ * "kdiag","vdiag","wk","wv","nk","nv","blk_start","blk_len","kcodes","vcodes"}. */
+int pkv_cache_buffer(pkv_cache* c, const char* name, void** ptr, int64_t* bytes);
+/* stream-ordered copy of bytes [offset, offset + n) of a named arena into a
+ * caller device buffer (export path for the reference-shaped state). */
+int pkv_cache_read(pkv_cache* c, const char* name, int64_t offset, int64_t n, void* dst, void* stream);
+
+/* quantize_group over n groups (quant.py:70-111): values fp64 concatenated with
+ * offsets[n+1] (device), outputs scale/zero [n] and unpacked codes. */
+int pkv_quantize_groups(const double* values, const int64_t* offsets, int32_t n, int32_t bits, double* scale,
+                        double* zero, uint8_t* codes, void* stream);
+/* pack_codes / unpack_codes (quant.py:120-179) on device buffers */
+int pkv_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out, void* stream);
+int pkv_unpack_codes(const uint8_t* packed, int64_t n, int32_t bits, uint8_t* codes, void* stream);
+/* match_many (patterns.py:206-221): x [n][D], patterns [P][D] fp64 device */
+int pkv_match(const double* x, int64_t n, const double* pat, int32_t P, int32_t D, int64_t* idx, double* dist,
+              double* residual, void* stream);
+/* midrange_center (patterns.py:161-171) */
+int pkv_midrange(const double* x, int64_t n, int32_t D, double* out, void* stream);
+/* lloyd_kmeans (patterns.py:72-126) on one point set: x device fp64 [T][D];
+ * outputs centers [k][D] fp64 (device), labels [T] int32 (device), history
+ * (host, 25) and counts; *n_centers = min(k, distinct rows). */
+int pkv_kmeans(const double* x, int64_t T, int32_t D, int32_t k, int64_t first_idx, double* centers,
+               int32_t* labels, double* history, int32_t* n_hist, int32_t* n_centers, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PKV_H_ */

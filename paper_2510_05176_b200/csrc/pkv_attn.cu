@@ -1,0 +1,432 @@
+// K3 decode_attn: softmax(q K^T * scale) V over the PatternKV cache of every
+// unit (new; the reference defines only the reconstruction it must equal,
+// engine.py:255-303 + the exact window, SPEC.md:318 has no attention).
+//
+// K is never materialised: with k_t = s_b*code_t + z_b + M[idx_t] (per-channel
+// block params s_b, z_b),
+//   q.k_t = (q o s_b).code_t + q.z_b + (q.M)[idx_t]
+// and with v_t = s_t*code_t + z_t + M'[idx_t] (per-token params),
+//   sum_t p_t v_t = sum_t (p_t s_t) code_t + (sum_t p_t z_t) 1 + sum_p W_p M'_p,
+// W_p = sum_{t: idx_t = p} p_t.  The code products run on tensor cores
+// (mma.m16n8k16, fp32 accumulate) with A fragments dequantized in registers
+// straight from one vector load of the fragment-ordered codes (LOP3 + HFMA2);
+// q o s and p o s are split hi+lo into two fp16 columns so the fp16 operand
+// rounding stays below 2^-22 relative.  Flash-decoding: CTA = chunk of blocks,
+// warp = stream of whole 128-token blocks, lazy online-softmax rescale; a
+// per-unit merge kernel adds the fp16 window exactly and combines chunks.
+#include "pkv_common.cuh"
+
+namespace pkv {
+
+constexpr int ATT_WARPS = 4;
+constexpr int ATT_THREADS = ATT_WARPS * 32;
+constexpr int MAXG = 8;         // GQA group size served (query heads per KV head)
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_TH = 8.f;  // lazy rescale threshold (log2 units)
+
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t lop3_magic(uint32_t w, uint32_t mask) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(mask), "r"(0x64006400u));  // (w & mask) | magic
+  return r;
+}
+__device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
+  return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+}
+
+// Dequantize slot s (0..16/bits-1) of a code word into a half2 of exact code values.
+template <int BITS>
+__device__ __forceinline__ uint32_t slot_h2(uint32_t w, int s) {
+  constexpr int PER = BITS == 2 ? 4 : (BITS == 4 ? 2 : 1);  // slots extractable without shifting
+  const uint32_t ww = s >= PER ? (w >> 8) : w;
+  const int ss = s >= PER ? s - PER : s;
+  const uint32_t mask = ((1u << BITS) - 1) * 0x00010001u << (ss * BITS);
+  const uint32_t v = lop3_magic(ww, mask);
+  // (1024 + 2^(ss*BITS) c) * 2^-(ss*BITS) - 1024 * 2^-(ss*BITS) = c exactly
+  const float sc = 1.f / (float)(1 << (ss * BITS));
+  const __half hs = __float2half_rn(sc), hb = __float2half_rn(-1024.f * sc);
+  return hfma2_u(v, pack_h2(hs, hs), pack_h2(hb, hb));
+}
+
+template <int BITS>
+__device__ __forceinline__ void load_words(const uint8_t* tile, int lane, uint32_t* w, int WL) {
+  constexpr int NW = 16 * BITS / 8;  // words per lane at Dp = 128
+  if (WL == NW) {
+    const uint4* p = reinterpret_cast<const uint4*>(tile) + lane * (NW / 4);
+#pragma unroll
+    for (int i = 0; i < NW / 4; ++i) {
+      uint4 v = __ldg(p + i);
+      w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+    }
+  } else {  // head_dim < 128: fewer words per lane
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(tile) + lane * WL;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) w[i] = i < WL ? __ldg(p + i) : 0u;
+  }
+}
+
+// A fragments of sub-tile j (4 half2 registers) from the lane's code words.
+template <int BITS>
+__device__ __forceinline__ void afrag(const uint32_t* w, int j, uint32_t* a) {
+  constexpr int S = 16 / BITS;
+#pragma unroll
+  for (int reg = 0; reg < 4; ++reg) {
+    const int R = 4 * j + reg;
+    a[reg] = slot_h2<BITS>(w[R / S], R % S);
+  }
+}
+
+template <int BITS, int NT>
+__global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kernel(DevCache c, AttnArgs a) {
+  const int u = blockIdx.y, chunk = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, qd = lane & 3;
+  const int Dp = c.Dp, D = c.D, G = a.G;
+  const int KT = Dp / 16;
+  const int WL = frag_words_per_lane(Dp, BITS);
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* sq = reinterpret_cast<float*>(smem_raw);                 // [MAXG][Dp]
+  float* sqm = sq + MAXG * Dp;                                     // [Pk][MAXG]
+  const int Pk = c.use_kp ? c.nk[u] : 0;
+  const int Pv = c.use_vp ? c.nv[u] : 0;
+  float* sW = sqm + (size_t)max(Pk, 1) * MAXG;                     // [warps][Pv][MAXG]
+  __half* sP = reinterpret_cast<__half*>(sW + (size_t)ATT_WARPS * max(Pv, 1) * MAXG);  // [warps][16][16]
+  float* sred = reinterpret_cast<float*>(sP + ATT_WARPS * 256);   // [warps][MAXG][4]
+
+  // ---- per-unit setup: q, q.M table, zeroed pattern weights -----------------------
+  for (int i = tid; i < MAXG * Dp; i += ATT_THREADS) {
+    const int h = i / Dp, ch = i - h * Dp;
+    sq[i] = (h < G && ch < D) ? a.q[((int64_t)u * G + h) * D + ch] : 0.f;
+  }
+  for (int i = tid; i < ATT_WARPS * max(Pv, 1) * MAXG; i += ATT_THREADS) sW[i] = 0.f;
+  __syncthreads();
+  for (int i = tid; i < Pk * MAXG; i += ATT_THREADS) {
+    const int p = i / MAXG, h = i - p * MAXG;
+    float s = 0.f;
+    if (h < G) {
+      const float* m = c.kpat32 + ((int64_t)u * c.Pcap + p) * Dp;
+      const float* qq = sq + h * Dp;
+      for (int ch = 0; ch < D; ++ch) s = fmaf(qq[ch], m[ch], s);
+    }
+    sqm[i] = s;
+  }
+  __syncthreads();
+
+  // ---- per-warp streaming state ----------------------------------------------------
+  float oacc[8][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) oacc[mt][nt][r] = 0.f;
+  float mrun[NT], lsum[NT], zsum[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) { mrun[nt] = -INFINITY; lsum[nt] = 0.f; zsum[nt] = 0.f; }
+  float* myW = sW + (size_t)warp * max(Pv, 1) * MAXG;
+  __half* myP = sP + warp * 256;
+
+  const int b0 = chunk * a.bpc;
+  const int b1 = min(a.nb, b0 + a.bpc);
+  for (int b = b0 + warp; b < b1; b += ATT_WARPS) {
+    const int L = c.blk_len[b];
+    const int64_t tstart = c.blk_start[b];
+    const float* kp = c.kparam32 + ((int64_t)u * c.NBcap + b) * 2 * Dp;
+    // B fragments of q o s_b (hi/lo columns) and q.z_b per head
+    uint32_t bq[8][NT][2];
+    float qz[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int col = 8 * nt + g, h = col >> 1, hl = col & 1;
+      float zpart = 0.f;
+#pragma unroll
+      for (int kt = 0; kt < 8; ++kt) {
+        if (kt < KT) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int ch = 16 * kt + 2 * qd + 8 * hh;
+            const float2 s2 = *reinterpret_cast<const float2*>(kp + ch);
+            const float2 z2 = *reinterpret_cast<const float2*>(kp + Dp + ch);
+            const float q0 = h < MAXG ? sq[h * Dp + ch] : 0.f, q1 = h < MAXG ? sq[h * Dp + ch + 1] : 0.f;
+            const float t0 = q0 * s2.x, t1 = q1 * s2.y;
+            const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
+            __half e0 = h0, e1 = h1;
+            if (hl) { e0 = __float2half_rn(t0 - __half2float(h0)); e1 = __float2half_rn(t1 - __half2float(h1)); }
+            bq[kt][nt][hh] = pack_h2(e0, e1);
+            zpart = fmaf(q0, z2.x, fmaf(q1, z2.y, zpart));
+          }
+        }
+      }
+      zpart += __shfl_xor_sync(0xffffffffu, zpart, 1);
+      zpart += __shfl_xor_sync(0xffffffffu, zpart, 2);
+      qz[nt] = __shfl_sync(0xffffffffu, zpart, 8 * qd);  // head 4nt+qd lives at g = 2qd
+    }
+
+    const uint8_t* kblk = c.kcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
+    const uint8_t* vblk = c.vcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
+    const int ntile = (L + 15) >> 4;
+    for (int ti = 0; ti < ntile; ++ti) {
+      const int tbytes = tile_bytes(Dp, BITS);
+      uint32_t kw[16 * BITS / 8], vw[16 * BITS / 8];
+      load_words<BITS>(kblk + ti * tbytes, lane, kw, WL);
+      load_words<BITS>(vblk + ti * tbytes, lane, vw, WL);
+      // token metadata for rows g, g+8
+      const int r0 = 16 * ti + g, r1 = r0 + 8;
+      const bool ok0 = r0 < L, ok1 = r1 < L;
+      const int64_t tk0 = (int64_t)u * c.Tcap + tstart + r0, tk1 = tk0 + 8;
+      const int ki0 = ok0 ? c.kidx[tk0] : -1, ki1 = ok1 ? c.kidx[tk1] : -1;
+      const int vi0 = ok0 ? c.vidx[tk0] : -1, vi1 = ok1 ? c.vidx[tk1] : -1;
+      const float2 vp0 = ok0 ? *reinterpret_cast<const float2*>(c.vparam32 + 2 * tk0) : make_float2(0.f, 0.f);
+      const float2 vp1 = ok1 ? *reinterpret_cast<const float2*>(c.vparam32 + 2 * tk1) : make_float2(0.f, 0.f);
+
+      // ---- S = K . (q o s): tokens on M, hi/lo head columns on N ----
+      float sacc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) sacc[nt][r] = 0.f;
+#pragma unroll
+      for (int kt = 0; kt < 8; ++kt) {
+        if (kt < KT) {
+          uint32_t af[4];
+          afrag<BITS>(kw, kt, af);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma16816(sacc[nt], af, bq[kt][nt][0], bq[kt][nt][1]);
+        }
+      }
+      // ---- online softmax (lazy rescale), P~ = p * s_t split hi/lo ----
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int h = 4 * nt + qd;
+        const float add0 = qz[nt] + (ki0 >= 0 ? sqm[ki0 * MAXG + min(h, MAXG - 1)] : 0.f);
+        const float add1 = qz[nt] + (ki1 >= 0 ? sqm[ki1 * MAXG + min(h, MAXG - 1)] : 0.f);
+        const float s0 = ok0 ? (sacc[nt][0] + sacc[nt][1] + add0) * a.scale_log2 : -INFINITY;
+        const float s1 = ok1 ? (sacc[nt][2] + sacc[nt][3] + add1) * a.scale_log2 : -INFINITY;
+        float tmax = fmaxf(s0, s1);
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+        if (tmax > mrun[nt] + RESCALE_TH || mrun[nt] == -INFINITY) {
+          const float mnew = fmaxf(tmax, mrun[nt]);
+          const float alpha = mrun[nt] == -INFINITY ? 0.f : exp2f(mrun[nt] - mnew);
+          lsum[nt] *= alpha;
+          zsum[nt] *= alpha;
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) oacc[mt][nt][r] *= alpha;
+          if (h < MAXG)
+            for (int p = g; p < Pv; p += 8) myW[p * MAXG + h] *= alpha;
+          mrun[nt] = mnew;
+        }
+        const float p0 = exp2f(s0 - mrun[nt]), p1 = exp2f(s1 - mrun[nt]);
+        lsum[nt] += p0 + p1;
+        zsum[nt] = fmaf(p0, vp0.y, fmaf(p1, vp1.y, zsum[nt]));
+        __syncwarp();  // rescaled W visible before other lanes add into it
+        if (h < MAXG) {
+          if (vi0 >= 0 && p0 != 0.f) atomicAdd(&myW[vi0 * MAXG + h], p0);
+          if (vi1 >= 0 && p1 != 0.f) atomicAdd(&myW[vi1 * MAXG + h], p1);
+        }
+        const float w0 = p0 * vp0.x, w1 = p1 * vp1.x;
+        const __half w0h = __float2half_rn(w0), w1h = __float2half_rn(w1);
+        const __half w0l = __float2half_rn(w0 - __half2float(w0h)), w1l = __float2half_rn(w1 - __half2float(w1h));
+        *reinterpret_cast<uint32_t*>(myP + g * 16 + 8 * nt + 2 * qd) = pack_h2(w0h, w0l);
+        *reinterpret_cast<uint32_t*>(myP + (g + 8) * 16 + 8 * nt + 2 * qd) = pack_h2(w1h, w1l);
+      }
+      __syncwarp();
+      // ---- O^T += V^T . P~ : channels on M ----
+      uint32_t bp[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int col = 8 * nt + g;
+        bp[nt][0] = pack_h2(myP[(2 * qd) * 16 + col], myP[(2 * qd + 1) * 16 + col]);
+        bp[nt][1] = pack_h2(myP[(2 * qd + 8) * 16 + col], myP[(2 * qd + 9) * 16 + col]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        if (mt < KT) {
+          uint32_t af[4];
+          afrag<BITS>(vw, mt, af);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma16816(oacc[mt][nt], af, bp[nt][0], bp[nt][1]);
+        }
+      }
+    }
+  }
+
+  // ---- merge the warps of the CTA --------------------------------------------------
+  // per-head running max m (same for the 8 lanes of a head), l and z partial per lane
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    float l = lsum[nt], z = zsum[nt];
+    l += __shfl_xor_sync(0xffffffffu, l, 4); l += __shfl_xor_sync(0xffffffffu, l, 8); l += __shfl_xor_sync(0xffffffffu, l, 16);
+    z += __shfl_xor_sync(0xffffffffu, z, 4); z += __shfl_xor_sync(0xffffffffu, z, 8); z += __shfl_xor_sync(0xffffffffu, z, 16);
+    const int h = 4 * nt + qd;
+    if (g == 0 && h < MAXG) {
+      sred[(warp * MAXG + h) * 4 + 0] = mrun[nt];
+      sred[(warp * MAXG + h) * 4 + 1] = l;
+      sred[(warp * MAXG + h) * 4 + 2] = z;
+    }
+  }
+  __syncthreads();
+  // global max per head and each warp's factor
+  float fac[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int h = min(4 * nt + qd, MAXG - 1);
+    float M = -INFINITY;
+    for (int w = 0; w < ATT_WARPS; ++w) M = fmaxf(M, sred[(w * MAXG + h) * 4]);
+    fac[nt] = (mrun[nt] == -INFINITY) ? 0.f : exp2f(mrun[nt] - M);
+  }
+  // O reduction buffer reuses sq: [MAXG][Dp] (q no longer needed)
+  __syncthreads();
+  for (int i = tid; i < MAXG * Dp; i += ATT_THREADS) sq[i] = 0.f;
+  __syncthreads();
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    if (mt < KT) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int h = 4 * nt + qd;
+        if (h < MAXG) {
+          atomicAdd(&sq[h * Dp + 16 * mt + g], (oacc[mt][nt][0] + oacc[mt][nt][1]) * fac[nt]);
+          atomicAdd(&sq[h * Dp + 16 * mt + g + 8], (oacc[mt][nt][2] + oacc[mt][nt][3]) * fac[nt]);
+        }
+      }
+    }
+  }
+  // pattern weights: W = sum_w fac_w W_w  (lanes of head h hold fac for their warp)
+  if (Pv > 0) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h = 4 * nt + qd;
+      if (h < MAXG)
+        for (int p = g; p < Pv; p += 8) myW[p * MAXG + h] *= fac[nt];
+    }
+  }
+  __syncthreads();
+  // final per-head sums and the pattern / zero-point terms, then write the partial
+  float* out = a.part + (((int64_t)u * a.nchunk + chunk) * G) * (Dp + 2);
+  for (int i = tid; i < G * Dp; i += ATT_THREADS) {
+    const int h = i / Dp, ch = i - h * Dp;
+    float M = -INFINITY, zt = 0.f;
+    for (int w = 0; w < ATT_WARPS; ++w) M = fmaxf(M, sred[(w * MAXG + h) * 4]);
+    for (int w = 0; w < ATT_WARPS; ++w) {
+      const float mw = sred[(w * MAXG + h) * 4];
+      if (mw != -INFINITY) zt += exp2f(mw - M) * sred[(w * MAXG + h) * 4 + 2];
+    }
+    float o = sq[i] + zt;
+    if (ch < D) {
+      for (int p = 0; p < Pv; ++p) {
+        float wsum = 0.f;
+        for (int w = 0; w < ATT_WARPS; ++w) wsum += sW[((size_t)w * max(Pv, 1) + p) * MAXG + h];
+        o = fmaf(wsum, c.vpat32[((int64_t)u * c.Pcap + p) * Dp + ch], o);
+      }
+    }
+    out[h * (Dp + 2) + ch] = o;
+    if (ch == 0) {
+      float l = 0.f;
+      for (int w = 0; w < ATT_WARPS; ++w) {
+        const float mw = sred[(w * MAXG + h) * 4];
+        if (mw != -INFINITY) l += exp2f(mw - M) * sred[(w * MAXG + h) * 4 + 1];
+      }
+      out[h * (Dp + 2) + Dp] = M;
+      out[h * (Dp + 2) + Dp + 1] = l;
+    }
+  }
+}
+
+// merge: exact fp32 attention over the window rows + combine chunk partials.
+// grid U, block 32*G threads (warp = head).
+template <typename T>
+__global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_slot0, float* out) {
+  const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (h >= a.G) return;
+  const int D = c.D, Dp = c.Dp;
+  const float* q = a.q + ((int64_t)u * a.G + h) * D;
+  float qv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) qv[j] = (lane + 32 * j < D) ? q[lane + 32 * j] : 0.f;
+  float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+  const T* wk = reinterpret_cast<const T*>(c.wk) + (int64_t)u * c.Wcap * D;
+  const T* wv = reinterpret_cast<const T*>(c.wv) + (int64_t)u * c.Wcap * D;
+  for (int r = 0; r < win_len; ++r) {
+    const int64_t row = (int64_t)((win_slot0 + r) % c.Wcap) * D;
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) s = fmaf(qv[j], (float)to_f64(wk[row + lane + 32 * j]), s);
+    s = warp_sum_f(s) * a.scale_log2;
+    const float mn = fmaxf(m, s);
+    const float al = m == -INFINITY ? 0.f : exp2f(m - mn);
+    const float p = exp2f(s - mn);
+    l = l * al + p;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = o[j] * al + (lane + 32 * j < D ? p * (float)to_f64(wv[row + lane + 32 * j]) : 0.f);
+    m = mn;
+  }
+  // combine with chunk partials
+  for (int ch = 0; ch < a.nchunk; ++ch) {
+    const float* pp = a.part + (((int64_t)u * a.nchunk + ch) * a.G + h) * (Dp + 2);
+    const float pm = pp[Dp], pl = pp[Dp + 1];
+    if (pm == -INFINITY) continue;
+    const float mn = fmaxf(m, pm);
+    const float al = m == -INFINITY ? 0.f : exp2f(m - mn), be = exp2f(pm - mn);
+    l = l * al + pl * be;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = o[j] * al + (lane + 32 * j < Dp ? pp[lane + 32 * j] * be : 0.f);
+    m = mn;
+  }
+  const float inv = 1.f / l;
+  float* dst = out + ((int64_t)u * a.G + h) * D;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) dst[lane + 32 * j] = o[j] * inv;
+}
+
+size_t attn_smem_bytes(int Dp, int Pk, int Pv) {
+  return (size_t)MAXG * Dp * 4 + (size_t)max(Pk, 1) * MAXG * 4 + (size_t)ATT_WARPS * max(Pv, 1) * MAXG * 4 +
+         ATT_WARPS * 256 * 2 + ATT_WARPS * MAXG * 4 * 4;
+}
+
+template <int BITS, int NT>
+static cudaError_t launch_chunks(const DevCache& c, const AttnArgs& a, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(attn_chunk_kernel<BITS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  attn_chunk_kernel<BITS, NT><<<dim3(a.nchunk, c.U), ATT_THREADS, smem, st>>>(c, a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_attn(const DevCache& c, const AttnArgs& a, int Pk_max, int Pv_max, int win_len, int win_slot0,
+                        float* out, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  if (a.nb > 0) {
+    size_t smem = attn_smem_bytes(c.Dp, Pk_max, Pv_max);
+    const int nt = a.G <= 4 ? 1 : 2;
+    if (c.bits == 2) e = nt == 1 ? launch_chunks<2, 1>(c, a, smem, st) : launch_chunks<2, 2>(c, a, smem, st);
+    else if (c.bits == 4) e = nt == 1 ? launch_chunks<4, 1>(c, a, smem, st) : launch_chunks<4, 2>(c, a, smem, st);
+    else e = nt == 1 ? launch_chunks<8, 1>(c, a, smem, st) : launch_chunks<8, 2>(c, a, smem, st);
+    if (e != cudaSuccess) return e;
+  }
+  AttnArgs a2 = a;
+  if (a.nb == 0) a2.nchunk = 0;
+  attn_merge_kernel<T><<<c.U, 32 * a.G, 0, st>>>(c, a2, win_len, win_slot0, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_attn<__half>(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
+template cudaError_t launch_attn<__nv_bfloat16>(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
+template cudaError_t launch_attn<float>(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
+template cudaError_t launch_attn<double>(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
+
+}  // namespace pkv

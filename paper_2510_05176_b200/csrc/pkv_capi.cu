@@ -1,0 +1,763 @@
+// C ABI of the B200 PatternKV codec (include/pkv.h): cache arenas, lockstep
+// lifecycle (prefill / append-and-refresh / decode attention / dequant) and
+// the group-level API.  Host logic mirrors engine.py:142-198 (geometry,
+// flush trigger, window retention) and gate.py:23-106 (threshold).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/pkv.h"
+#include "pkv_common.cuh"
+
+
+using namespace pkv;
+
+// ---------------------------------------------------------------------------------
+// errors (errors.py:9-14 taxonomy)
+// ---------------------------------------------------------------------------------
+static thread_local std::string g_err;
+static thread_local int64_t g_err_idx = -1;
+
+static int fail(int code, int64_t idx, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  g_err_idx = idx;
+  return code;
+}
+#define CU(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t _e = (x);                                                                      \
+    if (_e != cudaSuccess) return fail(PKV_CUDA, -1, "%s: %s", #x, cudaGetErrorString(_e));   \
+  } while (0)
+
+extern "C" int pkv_version(void) { return 1; }
+extern "C" const char* pkv_last_error(int64_t* index) {
+  if (index) *index = g_err_idx;
+  return g_err.c_str();
+}
+
+// ---------------------------------------------------------------------------------
+// gate constants (gate.py:23-106), host double arithmetic in the reference order
+// ---------------------------------------------------------------------------------
+static double horner(const double* c, int n, double r) {
+  double acc = c[n - 1];
+  for (int i = n - 2; i >= 0; --i) acc = acc * r + c[i];
+  return acc;
+}
+static const double kA[8] = {3.3871328727963666080e0, 1.3314166789178437745e2, 1.9715909503065514427e3, 1.3731693765509461125e4,
+                             4.5921953931549871457e4, 6.7265770927008700853e4, 3.3430575583588128105e4, 2.5090809287301226727e3};
+static const double kB[8] = {1.0, 4.2313330701600911252e1, 6.8718700749205790830e2, 5.3941960214247511077e3,
+                             2.1213794301586595867e4, 3.9307895800092710610e4, 2.8729085735721942674e4, 5.2264952788528545610e3};
+static const double kC[8] = {1.42343711074968357734e0, 4.63033784615654529590e0, 5.76949722146069140550e0, 3.64784832476320460504e0,
+                             1.27045825245236838258e0, 2.41780725177450611770e-1, 2.27238449892691845833e-2, 7.74545014278341407640e-4};
+static const double kD[8] = {1.0, 2.05319162663775882187e0, 1.67638483018380384940e0, 6.89767334985100004550e-1,
+                             1.48103976427480074590e-1, 1.51986665636164571966e-2, 5.47593808499534494600e-4, 1.05075007164441684324e-9};
+static const double kE[8] = {6.65790464350110377720e0, 5.46378491116411436990e0, 1.78482653991729133580e0, 2.96560571828504891230e-1,
+                             2.65321895265761230930e-2, 1.24266094738807843860e-3, 2.71155556874348757815e-5, 2.01033439929228813265e-7};
+static const double kF[8] = {1.0, 5.99832206555887937690e-1, 1.36929880922735805310e-1, 1.48753612908506148525e-2,
+                             7.86869131145613259100e-4, 1.84631831751005468180e-5, 1.42151175831644588870e-7, 2.04426310338993978564e-15};
+
+extern "C" int pkv_z_quantile(double alpha, double* out) {
+  if (!(alpha > 0.0 && alpha <= 0.5)) return fail(PKV_USAGE, -1, "alpha must lie in (0, 0.5], got %g", alpha);
+  const double q = alpha - 0.5;
+  double z;
+  if (std::fabs(q) <= 0.425) {
+    const double r = 0.180625 - q * q;
+    z = q * horner(kA, 8, r) / horner(kB, 8, r);
+  } else {
+    double r = q < 0 ? alpha : 1.0 - alpha;
+    r = std::sqrt(-std::log(r));
+    if (r <= 5.0) { r -= 1.6; z = horner(kC, 8, r) / horner(kD, 8, r); }
+    else { r -= 5.0; z = horner(kE, 8, r) / horner(kF, 8, r); }
+    if (q < 0) z = -z;
+  }
+  *out = -z;
+  return PKV_OK;
+}
+
+extern "C" int pkv_threshold(int32_t head_dim, double alpha, double* out) {
+  if (head_dim < 1) return fail(PKV_USAGE, -1, "head_dim must be >= 1, got %d", head_dim);
+  double z;
+  int rc = pkv_z_quantile(alpha, &z);
+  if (rc) return rc;
+  if (z <= 0.0) { *out = 1.0; return PKV_OK; }
+  const double c = 2.0 * z / std::sqrt(5.0 * head_dim);
+  if (c >= 1.0)
+    return fail(PKV_USAGE, -1, "no contraction ratio reaches significance for head_dim=%d, alpha=%g", head_dim, alpha);
+  double lo = 0.0, hi = 1.0;
+  while (hi - lo > 1e-12) {
+    const double mid = 0.5 * (lo + hi);
+    if ((1.0 - mid * mid) - c * std::sqrt(1.0 + std::pow(mid, 4)) >= 0.0) lo = mid;
+    else hi = mid;
+  }
+  *out = 0.5 * (lo + hi);
+  return PKV_OK;
+}
+
+extern "C" int pkv_config_validate(const pkv_config* c) {
+  if (!c) return fail(PKV_USAGE, -1, "null config");
+  if (c->bits != 2 && c->bits != 4 && c->bits != 8)
+    return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", c->bits);
+  if (c->pattern_count < 1) return fail(PKV_USAGE, -1, "pattern_count must be >= 1, got %d", c->pattern_count);
+  if (c->group_size < 1) return fail(PKV_USAGE, -1, "group_size must be >= 1, got %d", c->group_size);
+  if (c->residual_window < c->group_size)
+    return fail(PKV_USAGE, -1, "residual_window (%d) must be >= group_size (%d) so flushes always fill whole groups",
+                c->residual_window, c->group_size);
+  if (!(c->alpha > 0.0 && c->alpha <= 0.5)) return fail(PKV_USAGE, -1, "alpha must lie in (0, 0.5], got %g", c->alpha);
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// cache
+// ---------------------------------------------------------------------------------
+struct pkv_cache {
+  pkv_config cfg;
+  int U, D, Dp, dtype, esize, flags;
+  DevCache dev;
+  int64_t token_count = 0, committed = 0;
+  int win_len = 0, win_slot0 = 0, nb = 0;
+  int nb_prefill = 0;          // blocks laid out by prefill; later blocks are decode flushes of G
+  int64_t decode_base = 0;     // committed count after prefill
+  std::vector<int64_t> blk_start;
+  std::vector<int> blk_len;
+  int pk_bound = 0, pv_bound = 0;  // upper bounds of per-unit pattern counts
+  float* part = nullptr;
+  size_t part_bytes = 0;
+  unsigned* stats = nullptr;
+  unsigned long long* scratch_flag = nullptr;
+  int64_t uploaded_nbcap = -1, uploaded_base = -1;   // last block table sent to the device
+  std::vector<int64_t> uploaded_start;
+};
+
+static int esize_of(int dtype) {
+  switch (dtype) {
+    case PKV_F16: case PKV_BF16: return 2;
+    case PKV_F32: return 4;
+    case PKV_F64: return 8;
+    default: return 0;
+  }
+}
+
+template <typename P>
+static cudaError_t dalloc(P** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc((void**)p, bytes);
+  if (e != cudaSuccess) return e;
+  return cudaMemset(*p, 0, bytes);
+}
+
+// grow [U][old][row] -> [U][new][row]
+template <typename P>
+static cudaError_t regrow(P** p, int U, int64_t old_rows, int64_t new_rows, size_t row_bytes, cudaStream_t st) {
+  P* np_ = nullptr;
+  cudaError_t e = dalloc(&np_, (size_t)U * new_rows * row_bytes);
+  if (e != cudaSuccess) return e;
+  if (*p && old_rows > 0) {
+    e = cudaMemcpy2DAsync(np_, new_rows * row_bytes, *p, old_rows * row_bytes, old_rows * row_bytes, U,
+                          cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    cudaStreamSynchronize(st);
+  }
+  if (*p) cudaFree(*p);
+  *p = np_;
+  return cudaSuccess;
+}
+
+static int64_t nb_cap_for(int64_t Tcap, int G) { return (Tcap + G - 1) / G + 2; }
+
+// block table for every future decode flush is precomputed on the device, so a
+// flush needs no host->device traffic (CUDA-graph friendly)
+static int upload_blocks(pkv_cache* c, cudaStream_t st) {
+  const int G = c->cfg.group_size;
+  if (c->uploaded_nbcap == c->dev.NBcap && c->uploaded_start == c->blk_start && c->uploaded_base == c->decode_base)
+    return PKV_OK;
+  std::vector<int64_t> s(c->dev.NBcap);
+  std::vector<int> l(c->dev.NBcap);
+  for (int64_t b = 0; b < c->dev.NBcap; ++b) {
+    if (b < (int64_t)c->blk_start.size()) { s[b] = c->blk_start[b]; l[b] = c->blk_len[b]; }
+    else { s[b] = c->decode_base + (b - c->nb_prefill) * (int64_t)G; l[b] = G; }
+  }
+  CU(cudaMemcpyAsync(c->dev.blk_start, s.data(), s.size() * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(c->dev.blk_len, l.data(), l.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  c->uploaded_nbcap = c->dev.NBcap;
+  c->uploaded_start = c->blk_start;
+  c->uploaded_base = c->decode_base;
+  return PKV_OK;
+}
+
+static int reserve(pkv_cache* c, int64_t Tcap, int Pcap, cudaStream_t st) {
+  DevCache& d = c->dev;
+  const int U = c->U, D = c->D, Dp = c->Dp;
+  if (Pcap > 32767) return fail(PKV_USAGE, -1, "pattern table would exceed 32767 entries (16-bit indices)");
+  if (Pcap > d.Pcap) {
+    int64_t o = d.Pcap;
+    CU(regrow(&d.kpat64, U, o, Pcap, (size_t)D * 8, st));
+    CU(regrow(&d.vpat64, U, o, Pcap, (size_t)D * 8, st));
+    CU(regrow(&d.kpat32, U, o, Pcap, (size_t)Dp * 4, st));
+    CU(regrow(&d.vpat32, U, o, Pcap, (size_t)Dp * 4, st));
+    d.Pcap = Pcap;
+  }
+  if (Tcap > d.Tcap) {
+    const int64_t oT = d.Tcap, oNB = d.NBcap;
+    const int64_t nNB = nb_cap_for(Tcap, d.G);
+    CU(regrow(&d.kidx, U, oT, Tcap, 2, st));
+    CU(regrow(&d.vidx, U, oT, Tcap, 2, st));
+    CU(regrow(&d.vparam32, U, oT, Tcap, 8, st));
+    CU(regrow(&d.vparam64, U, oT, Tcap, 16, st));
+    if (d.keep_diag) {
+      CU(regrow(&d.kdiag, U, oT, Tcap, 16, st));
+      CU(regrow(&d.vdiag, U, oT, Tcap, 16, st));
+    }
+    CU(regrow(&d.kcodes, U, oNB, nNB, (size_t)d.blk_bytes, st));
+    CU(regrow(&d.vcodes, U, oNB, nNB, (size_t)d.blk_bytes, st));
+    CU(regrow(&d.kparam32, U, oNB, nNB, (size_t)2 * Dp * 4, st));
+    CU(regrow(&d.kparam64, U, oNB, nNB, (size_t)2 * D * 8, st));
+    CU(regrow(&d.blk_start, 1, oNB, nNB, 8, st));
+    CU(regrow(&d.blk_len, 1, oNB, nNB, 4, st));
+    d.Tcap = Tcap;
+    d.NBcap = nNB;
+    int rc = upload_blocks(c, st);
+    if (rc) return rc;
+  }
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t head_dim, int32_t in_dtype,
+                                int64_t max_tokens, int32_t max_patterns, int32_t flags, pkv_cache** out) {
+  int rc = pkv_config_validate(cfg);
+  if (rc) return rc;
+  if (n_units < 1) return fail(PKV_USAGE, -1, "n_units must be >= 1, got %d", n_units);
+  if (head_dim < 1 || head_dim > DMAX)
+    return fail(PKV_USAGE, -1, "head_dim must lie in [1, %d] on the B200 path, got %d", DMAX, head_dim);
+  if (cfg->group_size > GMAX)
+    return fail(PKV_USAGE, -1, "group_size must be <= %d on the B200 path, got %d", GMAX, cfg->group_size);
+  if (cfg->pattern_count > 96)
+    return fail(PKV_USAGE, -1, "pattern_count must be <= 96 on the B200 path, got %d", cfg->pattern_count);
+  if (!esize_of(in_dtype)) return fail(PKV_USAGE, -1, "unknown dtype code %d", in_dtype);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PKV_USAGE, -1, "no CUDA device: the PatternKV B200 codec has no CPU fallback");
+  double thr = 1.0;
+  rc = pkv_threshold(head_dim, cfg->alpha, &thr);
+  if (rc && (cfg->use_v_gate || cfg->use_k_gate)) return rc;
+
+  pkv_cache* c = new pkv_cache();
+  c->cfg = *cfg;
+  c->U = n_units;
+  c->D = head_dim;
+  c->Dp = round_up(head_dim, 32);
+  c->dtype = in_dtype;
+  c->esize = esize_of(in_dtype);
+  c->flags = flags;
+  DevCache& d = c->dev;
+  std::memset(&d, 0, sizeof d);
+  d.U = n_units; d.D = head_dim; d.Dp = c->Dp; d.bits = cfg->bits; d.qmax = (1 << cfg->bits) - 1;
+  d.G = cfg->group_size; d.W = cfg->residual_window; d.Wcap = cfg->residual_window + cfg->group_size;
+  d.ntile_blk = (cfg->group_size + 15) / 16;
+  d.blk_bytes = d.ntile_blk * tile_bytes(c->Dp, cfg->bits);
+  d.in_dtype = in_dtype;
+  d.use_kp = cfg->use_k_patterns; d.use_vp = cfg->use_v_patterns; d.use_vgate = cfg->use_v_gate;
+  d.use_kgate = cfg->use_k_gate; d.gen_new = cfg->generate_new_patterns;
+  d.keep_diag = (flags & PKV_FLAG_DECISIONS) ? 1 : 0;
+  d.thr = thr;
+  cudaStream_t st = 0;
+  auto bail = [&](int code) { pkv_cache_destroy(c); return code; };
+  if (dalloc(&d.kpmax, (size_t)n_units * 4) || dalloc(&d.vpmax, (size_t)n_units * 4) ||
+      dalloc(&d.nk, (size_t)n_units * 4) || dalloc(&d.nv, (size_t)n_units * 4) ||
+      dalloc(&d.wk, (size_t)n_units * d.Wcap * head_dim * c->esize) ||
+      dalloc(&d.wv, (size_t)n_units * d.Wcap * head_dim * c->esize) || dalloc(&c->scratch_flag, 8))
+    return bail(fail(PKV_CUDA, -1, "cudaMalloc failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if (flags & PKV_FLAG_STATS) {
+    if (dalloc(&c->stats, 16)) return bail(fail(PKV_CUDA, -1, "cudaMalloc failed"));
+    d.stats = c->stats;
+  }
+  rc = reserve(c, std::max<int64_t>(max_tokens, 1), std::max(max_patterns, cfg->pattern_count + 8), st);
+  if (rc) return bail(rc);
+  *out = c;
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_destroy(pkv_cache* c) {
+  if (!c) return PKV_OK;
+  DevCache& d = c->dev;
+  void* ptrs[] = {d.kpat64, d.vpat64, d.kpat32, d.vpat32, d.kpmax, d.vpmax, d.nk, d.nv, d.blk_start, d.blk_len,
+                  d.kcodes, d.kparam32, d.kparam64, d.kidx, d.vcodes, d.vparam32, d.vparam64, d.vidx, d.kdiag,
+                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_info_get(pkv_cache* c, pkv_cache_info* o) {
+  if (!c || !o) return fail(PKV_USAGE, -1, "null argument");
+  o->n_units = c->U; o->head_dim = c->D; o->head_dim_padded = c->Dp; o->in_dtype = c->dtype;
+  o->token_count = c->token_count; o->committed_count = c->committed;
+  o->window_len = c->win_len; o->window_slot0 = c->win_slot0; o->n_blocks = c->nb;
+  o->pattern_capacity = c->dev.Pcap; o->token_capacity = c->dev.Tcap; o->block_bytes = c->dev.blk_bytes;
+  o->n_refined = 0; o->n_exact_div = 0;
+  if (c->stats) {
+    unsigned s[4];
+    CU(cudaMemcpy(s, c->stats, 16, cudaMemcpyDeviceToHost));
+    o->n_refined = s[0]; o->n_exact_div = s[1];
+  }
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_reserve(pkv_cache* c, int64_t max_tokens, int32_t max_patterns, void* stream) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  return reserve(c, std::max(max_tokens, c->dev.Tcap), std::max<int>(max_patterns, c->dev.Pcap), (cudaStream_t)stream);
+}
+
+extern "C" int pkv_cache_reset(pkv_cache* c, int32_t keep_patterns, void* stream) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  cudaStream_t st = (cudaStream_t)stream;
+  c->token_count = 0;
+  c->committed = 0;
+  c->win_len = 0;
+  c->win_slot0 = 0;
+  c->nb = 0;
+  if (!keep_patterns) {
+    CU(cudaMemsetAsync(c->dev.nk, 0, (size_t)c->U * 4, st));
+    CU(cudaMemsetAsync(c->dev.nv, 0, (size_t)c->U * 4, st));
+    CU(cudaMemsetAsync(c->dev.kpmax, 0, (size_t)c->U * 4, st));
+    CU(cudaMemsetAsync(c->dev.vpmax, 0, (size_t)c->U * 4, st));
+    c->pk_bound = c->pv_bound = 0;
+  }
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_buffer(pkv_cache* c, const char* name, void** ptr, int64_t* bytes) {
+  if (!c || !name || !ptr) return fail(PKV_USAGE, -1, "null argument");
+  DevCache& d = c->dev;
+  const int64_t U = c->U, T = d.Tcap, NB = d.NBcap, P = d.Pcap, D = c->D;
+  struct { const char* n; void* p; int64_t b; } tab[] = {
+      {"kpat64", d.kpat64, U * P * D * 8}, {"vpat64", d.vpat64, U * P * D * 8},
+      {"kparam64", d.kparam64, U * NB * 2 * D * 8}, {"vparam64", d.vparam64, U * T * 16},
+      {"kidx", d.kidx, U * T * 2}, {"vidx", d.vidx, U * T * 2},
+      {"kdiag", d.kdiag, d.keep_diag ? U * T * 16 : 0}, {"vdiag", d.vdiag, d.keep_diag ? U * T * 16 : 0},
+      {"wk", d.wk, U * d.Wcap * D * c->esize}, {"wv", d.wv, U * d.Wcap * D * c->esize},
+      {"nk", d.nk, U * 4}, {"nv", d.nv, U * 4}, {"blk_start", d.blk_start, NB * 8}, {"blk_len", d.blk_len, NB * 4},
+      {"kcodes", d.kcodes, U * NB * d.blk_bytes}, {"vcodes", d.vcodes, U * NB * d.blk_bytes},
+      {"kparam32", d.kparam32, U * NB * 2 * d.Dp * 4}, {"vparam32", d.vparam32, U * T * 8},
+      {"kpat32", d.kpat32, U * P * d.Dp * 4}, {"vpat32", d.vpat32, U * P * d.Dp * 4},
+  };
+  for (auto& e : tab) {
+    if (std::strcmp(e.n, name) == 0) {
+      *ptr = e.p;
+      if (bytes) *bytes = e.b;
+      return PKV_OK;
+    }
+  }
+  return fail(PKV_USAGE, -1, "unknown buffer name '%s'", name);
+}
+
+extern "C" int pkv_cache_read(pkv_cache* c, const char* name, int64_t offset, int64_t n, void* dst, void* stream) {
+  void* p = nullptr;
+  int64_t bytes = 0;
+  int rc = pkv_cache_buffer(c, name, &p, &bytes);
+  if (rc) return rc;
+  if (offset < 0 || n < 0 || offset + n > bytes)
+    return fail(PKV_USAGE, offset, "read [%lld, %lld) outside arena '%s' of %lld bytes", (long long)offset,
+                (long long)(offset + n), name, (long long)bytes);
+  if (n) CU(cudaMemcpyAsync(dst, (const char*)p + offset, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// finiteness (engine.py:132-139)
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_check_finite(const void* x, int32_t dtype, int64_t n, int64_t* first_bad, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* flag = nullptr;
+  CU(cudaMallocAsync((void**)&flag, 8, st));
+  CU(cudaMemsetAsync(flag, 0xff, 8, st));
+  cudaError_t e;
+  switch (dtype) {
+    case PKV_F16: e = launch_finite((const __half*)x, n, flag, st); break;
+    case PKV_BF16: e = launch_finite((const __nv_bfloat16*)x, n, flag, st); break;
+    case PKV_F32: e = launch_finite((const float*)x, n, flag, st); break;
+    case PKV_F64: e = launch_finite((const double*)x, n, flag, st); break;
+    default: cudaFreeAsync(flag, st); return fail(PKV_USAGE, -1, "unknown dtype code %d", dtype);
+  }
+  CU(e);
+  unsigned long long h = ~0ull;
+  CU(cudaMemcpyAsync(&h, flag, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaFreeAsync(flag, st));
+  CU(cudaStreamSynchronize(st));
+  *first_bad = h == ~0ull ? -1 : (int64_t)h;
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// dtype dispatch helper
+// ---------------------------------------------------------------------------------
+template <typename F>
+static cudaError_t dispatch(int dtype, F&& f) {
+  switch (dtype) {
+    case PKV_F16: return f((__half*)nullptr);
+    case PKV_BF16: return f((__nv_bfloat16*)nullptr);
+    case PKV_F32: return f((float*)nullptr);
+    default: return f((double*)nullptr);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// mining (patterns.py:145-158 per unit)
+// ---------------------------------------------------------------------------------
+static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv, int64_t T, const int64_t* fk,
+                     const int64_t* fv, double* hist_host, int32_t* niter_host, cudaStream_t st) {
+  const int U = c->U, k = c->cfg.pattern_count;
+  if (T < 1) return fail(PKV_USAGE, -1, "pattern mining expects a non-empty 2-D array of row vectors");
+  for (int s = 0; s < 2; ++s) {
+    const int64_t* f = s == 0 ? fk : fv;
+    if (!((side_mask >> s) & 1)) continue;
+    for (int u = 0; u < U; ++u)
+      if (f[u] < 0 || f[u] >= T) return fail(PKV_USAGE, f[u], "first seed index %lld outside [0, %lld)", (long long)f[u], (long long)T);
+  }
+  int rc = reserve(c, c->dev.Tcap, std::max(c->dev.Pcap, k + 8), st);
+  if (rc) return rc;
+  const size_t n2 = (size_t)U * 2 * T;
+  double *near_ = nullptr, *own = nullptr, *hist = nullptr;
+  int *lab = nullptr, *lab2 = nullptr, *list = nullptr, *niter = nullptr;
+  int64_t* first = nullptr;
+  CU(cudaMallocAsync((void**)&near_, n2 * 8, st));
+  CU(cudaMallocAsync((void**)&own, n2 * 8, st));
+  CU(cudaMallocAsync((void**)&lab, n2 * 4, st));
+  CU(cudaMallocAsync((void**)&lab2, n2 * 4, st));
+  CU(cudaMallocAsync((void**)&list, n2 * 4, st));
+  CU(cudaMallocAsync((void**)&hist, (size_t)U * 2 * 25 * 8, st));
+  CU(cudaMallocAsync((void**)&niter, (size_t)U * 2 * 4, st));
+  CU(cudaMallocAsync((void**)&first, (size_t)U * 2 * 8, st));
+  std::vector<int64_t> fh((size_t)U * 2, 0);
+  for (int u = 0; u < U; ++u) {
+    if (side_mask & 1) fh[u] = fk[u];
+    if (side_mask & 2) fh[U + u] = fv[u];
+  }
+  CU(cudaMemcpyAsync(first, fh.data(), fh.size() * 8, cudaMemcpyHostToDevice, st));
+  cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
+    using T_ = std::remove_pointer_t<decltype(tp)>;
+    MineArgs<T_> a;
+    a.x[0] = (const T_*)xk; a.x[1] = (const T_*)xv;
+    a.unit_stride = T * c->D; a.T = T;
+    a.first[0] = first; a.first[1] = first + U;
+    a.k = k; a.side_mask = side_mask;
+    a.near_ = near_; a.own = own; a.lab = lab; a.lab2 = lab2; a.list = list;
+    a.hist = hist; a.niter = niter; a.labels_out = nullptr;
+    return launch_mine<T_>(c->dev, a, st);
+  });
+  CU(e);
+  if (hist_host || niter_host) {
+    std::vector<double> hh((size_t)U * 2 * 25);
+    std::vector<int> nh((size_t)U * 2);
+    CU(cudaMemcpyAsync(hh.data(), hist, hh.size() * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(nh.data(), niter, nh.size() * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const int s = (side_mask & 1) ? 0 : 1;
+    for (int u = 0; u < U; ++u) {
+      if (hist_host) std::memcpy(hist_host + (size_t)u * 25, hh.data() + ((size_t)u * 2 + s) * 25, 25 * 8);
+      if (niter_host) niter_host[u] = nh[(size_t)u * 2 + s];
+    }
+  }
+  for (void* p : {(void*)near_, (void*)own, (void*)lab, (void*)lab2, (void*)list, (void*)hist, (void*)niter, (void*)first})
+    CU(cudaFreeAsync(p, st));
+  if (side_mask & 1) c->pk_bound = k;
+  if (side_mask & 2) c->pv_bound = k;
+  return PKV_OK;
+}
+
+extern "C" int pkv_mine(pkv_cache* c, int32_t side, const void* x, int64_t T, const int64_t* first_idx, double* history,
+                        int32_t* niter, void* stream) {
+  if (!c || !x || !first_idx) return fail(PKV_USAGE, -1, "null argument");
+  if (side != 0 && side != 1) return fail(PKV_USAGE, -1, "side must be 0 (K) or 1 (V)");
+  return mine_impl(c, 1 << side, x, x, T, first_idx, first_idx, history, niter, (cudaStream_t)stream);
+}
+
+extern "C" int pkv_set_patterns(pkv_cache* c, int32_t side, const double* pat, int32_t P, void* stream) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  if (P < 0) return fail(PKV_USAGE, -1, "negative pattern count");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = reserve(c, c->dev.Tcap, std::max(c->dev.Pcap, P + 8), st);
+  if (rc) return rc;
+  DevCache& d = c->dev;
+  double* p64 = side == 0 ? d.kpat64 : d.vpat64;
+  float* p32 = side == 0 ? d.kpat32 : d.vpat32;
+  std::vector<double> h((size_t)c->U * P * c->D);
+  if (P > 0) CU(cudaMemcpyAsync(h.data(), pat, h.size() * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::vector<double> h64((size_t)c->U * d.Pcap * c->D, 0.0);
+  std::vector<float> h32((size_t)c->U * d.Pcap * d.Dp, 0.f);
+  std::vector<float> pm(c->U, 0.f);
+  std::vector<int> n(c->U, P);
+  for (int u = 0; u < c->U; ++u)
+    for (int p = 0; p < P; ++p)
+      for (int ch = 0; ch < c->D; ++ch) {
+        const double v = h[((size_t)u * P + p) * c->D + ch];
+        h64[((size_t)u * d.Pcap + p) * c->D + ch] = v;
+        h32[((size_t)u * d.Pcap + p) * d.Dp + ch] = (float)v;
+        pm[u] = std::max(pm[u], (float)std::fabs(v) * (1.f + 1e-6f));
+      }
+  CU(cudaMemcpyAsync(p64, h64.data(), h64.size() * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(p32, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(side == 0 ? d.kpmax : d.vpmax, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(side == 0 ? d.nk : d.nv, n.data(), n.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  if (side == 0) c->pk_bound = P; else c->pv_bound = P;
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// prefill (engine.py:142-169)
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T, const int64_t* first_k,
+                           const int64_t* first_v, void* stream) {
+  if (!c || !k || !v) return fail(PKV_USAGE, -1, "null argument");
+  if (T < 1) return fail(PKV_USAGE, -1, "prefill K must be a non-empty (tokens, dim) matrix");
+  if (c->token_count != 0) return fail(PKV_USAGE, -1, "prefill on a cache that already holds %lld tokens", (long long)c->token_count);
+  cudaStream_t st = (cudaStream_t)stream;
+  const pkv_config& cfg = c->cfg;
+  const int W = cfg.residual_window, G = cfg.group_size;
+  const int64_t commit_n = T - std::min<int64_t>(T, W);
+  int rc = reserve(c, std::max<int64_t>(c->dev.Tcap, T + 4 * G), c->dev.Pcap, st);
+  if (rc) return rc;
+  // mining (engine.py:156-159)
+  int mask = 0;
+  if (cfg.use_k_patterns && first_k) mask |= 1;
+  if (cfg.use_v_patterns && first_v) mask |= 2;
+  if (mask) {
+    rc = mine_impl(c, mask, k, v, T, first_k, first_v, nullptr, nullptr, st);
+    if (rc) return rc;
+  }
+  // block geometry (engine.py:161-165): spans of G from 0, short tail allowed
+  c->blk_start.clear();
+  c->blk_len.clear();
+  for (int64_t s = 0; s < commit_n; s += G) {
+    c->blk_start.push_back(s);
+    c->blk_len.push_back((int)std::min<int64_t>(G, commit_n - s));
+  }
+  c->nb = c->nb_prefill = (int)c->blk_start.size();
+  c->decode_base = commit_n;
+  rc = upload_blocks(c, st);
+  if (rc) return rc;
+  cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
+    using T_ = std::remove_pointer_t<decltype(tp)>;
+    SpanSrc<T_> sk{(const T_*)k, T * c->D, 0, INT64_MAX / 4};
+    SpanSrc<T_> sv{(const T_*)v, T * c->D, 0, INT64_MAX / 4};
+    cudaError_t e1 = launch_encode<T_>(c->dev, sk, sv, 0, c->nb, st);
+    if (e1 != cudaSuccess) return e1;
+    // window = newest min(T, W) rows (engine.py:166-167)
+    const size_t off = (size_t)commit_n * c->D;
+    return launch_window_put<T_>(c->dev, (const T_*)k + off, (const T_*)v + off, T * c->D, (int)(T - commit_n), 0, st);
+  });
+  CU(e);
+  c->win_slot0 = 0;
+  c->win_len = (int)(T - commit_n);
+  c->token_count = T;
+  c->committed = commit_n;
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// append-and-refresh (engine.py:172-198)
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stream) {
+  if (!c || !k || !v) return fail(PKV_USAGE, -1, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const pkv_config& cfg = c->cfg;
+  const int W = cfg.residual_window, G = cfg.group_size;
+  DevCache& d = c->dev;
+  const int slot = (c->win_slot0 + c->win_len) % d.Wcap;
+  cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
+    using T_ = std::remove_pointer_t<decltype(tp)>;
+    return launch_window_put<T_>(d, (const T_*)k, (const T_*)v, c->D, 1, slot, st);
+  });
+  CU(e);
+  c->win_len += 1;
+  c->token_count += 1;
+  if (c->win_len == W + G) {
+    // capacity for one more block and one more pattern per side
+    const bool grow_p = cfg.generate_new_patterns;
+    int need_p = std::max(c->pk_bound, c->pv_bound) + (grow_p ? 1 : 0);
+    if (c->committed + G > d.Tcap || c->nb + 1 > d.NBcap - 1 || need_p > d.Pcap) {
+      int rc = reserve(c, std::max<int64_t>(d.Tcap * 2, c->committed + 2 * G),
+                       need_p > d.Pcap ? std::max(2 * d.Pcap, need_p) : d.Pcap, st);
+      if (rc) return rc;
+    }
+    if (grow_p) {
+      int mask = (cfg.use_k_patterns ? 1 : 0) | (cfg.use_v_patterns ? 2 : 0);
+      if (mask) {
+        e = dispatch(c->dtype, [&](auto* tp) {
+          using T_ = std::remove_pointer_t<decltype(tp)>;
+          return launch_refresh<T_>(d, c->win_slot0, G, mask, st);
+        });
+        CU(e);
+        if (mask & 1) c->pk_bound += 1;
+        if (mask & 2) c->pv_bound += 1;
+      }
+    }
+    // commit the oldest G rows against the refreshed tables (engine.py:195)
+    e = dispatch(c->dtype, [&](auto* tp) {
+      using T_ = std::remove_pointer_t<decltype(tp)>;
+      SpanSrc<T_> sk{(const T_*)d.wk, (int64_t)d.Wcap * c->D, c->win_slot0, d.Wcap};
+      SpanSrc<T_> sv{(const T_*)d.wv, (int64_t)d.Wcap * c->D, c->win_slot0, d.Wcap};
+      return launch_encode<T_>(d, sk, sv, c->nb, 1, st);
+    });
+    CU(e);
+    c->blk_start.push_back(c->committed);
+    c->blk_len.push_back(G);
+    c->nb += 1;
+    c->committed += G;
+    c->win_slot0 = (c->win_slot0 + G) % d.Wcap;
+    c->win_len -= G;
+  }
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// decode attention
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_decode_attn(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, float* out, void* stream) {
+  if (!c || !q || !out) return fail(PKV_USAGE, -1, "null argument");
+  if (gqa < 1 || gqa > 8) return fail(PKV_USAGE, -1, "query heads per KV head must lie in [1, 8], got %d", gqa);
+  if (c->token_count == 0) return fail(PKV_USAGE, -1, "attention over an empty cache");
+  cudaStream_t st = (cudaStream_t)stream;
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  AttnArgs a;
+  a.q = q; a.G = gqa; a.scale_log2 = sm_scale * 1.4426950408889634f; a.nb = c->nb;
+  // enough CTAs for ~4 waves at 4 CTAs/SM, >= 4 blocks per chunk (one per warp)
+  const int target = 16 * num_sms;
+  int nchunk = std::max(1, std::min((target + c->U - 1) / c->U, (c->nb + 3) / 4));
+  a.bpc = std::max(1, (c->nb + nchunk - 1) / nchunk);
+  a.nchunk = std::max(1, (c->nb + a.bpc - 1) / a.bpc);
+  const size_t need = (size_t)c->U * a.nchunk * gqa * (c->Dp + 2) * 4;
+  if (need > c->part_bytes) {
+    if (c->part) cudaFree(c->part);
+    CU(cudaMalloc((void**)&c->part, need));
+    c->part_bytes = need;
+  }
+  a.part = c->part;
+  const int pk = c->cfg.use_k_patterns ? c->pk_bound : 0, pv = c->cfg.use_v_patterns ? c->pv_bound : 0;
+  cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
+    using T_ = std::remove_pointer_t<decltype(tp)>;
+    return launch_attn<T_>(c->dev, a, pk, pv, c->win_len, c->win_slot0, out, st);
+  });
+  CU(e);
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// reconstruction / export
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_dequant(pkv_cache* c, int64_t t0, int64_t t1, double* k_out, double* v_out, void* stream) {
+  if (!c || ((!k_out || !v_out) && t1 > t0)) return fail(PKV_USAGE, -1, "null argument");
+  if (t0 < 0 || t1 > c->committed || t0 > t1)
+    return fail(PKV_USAGE, t0, "token range [%lld, %lld) outside committed [0, %lld)", (long long)t0, (long long)t1,
+                (long long)c->committed);
+  CU(launch_dequant(c->dev, c->nb, t0, t1 - t0, k_out, v_out, (cudaStream_t)stream));
+  return PKV_OK;
+}
+
+extern "C" int pkv_export_codes(pkv_cache* c, int64_t t0, int64_t t1, uint8_t* kc, uint8_t* vc, void* stream) {
+  if (!c || ((!kc || !vc) && t1 > t0)) return fail(PKV_USAGE, -1, "null argument");
+  if (t0 < 0 || t1 > c->committed || t0 > t1) return fail(PKV_USAGE, t0, "token range outside committed tokens");
+  CU(launch_codes(c->dev, c->nb, t0, t1 - t0, kc, vc, (cudaStream_t)stream));
+  return PKV_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// group-level API
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_quantize_groups(const double* values, const int64_t* offsets, int32_t n, int32_t bits, double* scale,
+                                   double* zero, uint8_t* codes, void* stream) {
+  if (bits != 2 && bits != 4 && bits != 8)
+    return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", bits);
+  CU(launch_quantize_groups(values, offsets, n, bits, scale, zero, codes, (cudaStream_t)stream));
+  return PKV_OK;
+}
+extern "C" int pkv_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out, void* stream) {
+  if (bits != 2 && bits != 4 && bits != 8)
+    return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", bits);
+  CU(launch_pack(codes, n, bits, out, (cudaStream_t)stream));
+  return PKV_OK;
+}
+extern "C" int pkv_unpack_codes(const uint8_t* packed, int64_t n, int32_t bits, uint8_t* codes, void* stream) {
+  if (bits != 2 && bits != 4 && bits != 8)
+    return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", bits);
+  CU(launch_unpack(packed, n, bits, codes, (cudaStream_t)stream));
+  return PKV_OK;
+}
+extern "C" int pkv_match(const double* x, int64_t n, const double* pat, int32_t P, int32_t D, int64_t* idx, double* dist,
+                         double* residual, void* stream) {
+  if (P < 1) return fail(PKV_USAGE, -1, "cannot match against an empty pattern set");
+  CU(launch_match(x, n, pat, P, D, idx, dist, residual, (cudaStream_t)stream));
+  return PKV_OK;
+}
+extern "C" int pkv_midrange(const double* x, int64_t n, int32_t D, double* out, void* stream) {
+  if (n < 1) return fail(PKV_USAGE, -1, "window must be a non-empty 2-D array of row vectors");
+  CU(launch_midrange(x, n, D, out, (cudaStream_t)stream));
+  return PKV_OK;
+}
+
+extern "C" int pkv_kmeans(const double* x, int64_t T, int32_t D, int32_t k, int64_t first_idx, double* centers,
+                          int32_t* labels, double* history, int32_t* n_hist, int32_t* n_centers, void* stream) {
+  if (T < 1) return fail(PKV_USAGE, -1, "k-means expects a non-empty 2-D array of row vectors");
+  if (k < 1) return fail(PKV_USAGE, -1, "cluster count must be >= 1, got %d", k);
+  if (k > 96) return fail(PKV_USAGE, -1, "cluster count must be <= 96 on the B200 path, got %d", k);
+  if (D < 1 || D > 1024) return fail(PKV_USAGE, -1, "vector dimension must lie in [1, 1024], got %d", D);
+  if (first_idx < 0 || first_idx >= T) return fail(PKV_USAGE, first_idx, "first seed index outside the point set");
+  cudaStream_t st = (cudaStream_t)stream;
+  DevCache d;
+  std::memset(&d, 0, sizeof d);
+  d.U = 1; d.D = D; d.Dp = round_up(D, 32); d.Pcap = k;
+  d.kpat64 = centers;
+  CU(cudaMallocAsync((void**)&d.kpat32, (size_t)k * d.Dp * 4, st));
+  CU(cudaMallocAsync((void**)&d.kpmax, 4, st));
+  CU(cudaMallocAsync((void**)&d.nk, 4, st));
+  const size_t n2 = (size_t)2 * T;
+  MineArgs<double> a;
+  a.x[0] = x; a.x[1] = x; a.unit_stride = T * D; a.T = T;
+  int64_t* first = nullptr;
+  CU(cudaMallocAsync((void**)&first, 16, st));
+  int64_t fh[2] = {first_idx, first_idx};
+  CU(cudaMemcpyAsync(first, fh, 16, cudaMemcpyHostToDevice, st));
+  a.first[0] = first; a.first[1] = first;
+  a.k = k; a.side_mask = 1;
+  CU(cudaMallocAsync((void**)&a.near_, n2 * 8, st));
+  CU(cudaMallocAsync((void**)&a.own, n2 * 8, st));
+  CU(cudaMallocAsync((void**)&a.lab, n2 * 4, st));
+  CU(cudaMallocAsync((void**)&a.lab2, n2 * 4, st));
+  CU(cudaMallocAsync((void**)&a.list, n2 * 4, st));
+  CU(cudaMallocAsync((void**)&a.hist, 2 * 25 * 8, st));
+  CU(cudaMallocAsync((void**)&a.niter, 8, st));
+  a.labels_out = labels;
+  CU(launch_mine<double>(d, a, st));
+  int nc = 0, ni = 0;
+  CU(cudaMemcpyAsync(&nc, d.nk, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&ni, a.niter, 4, cudaMemcpyDeviceToHost, st));
+  if (history) CU(cudaMemcpyAsync(history, a.hist, 25 * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (void* p : {(void*)d.kpat32, (void*)d.kpmax, (void*)d.nk, (void*)first, (void*)a.near_, (void*)a.own, (void*)a.lab,
+                  (void*)a.lab2, (void*)a.list, (void*)a.hist, (void*)a.niter})
+    CU(cudaFreeAsync(p, st));
+  if (n_hist) *n_hist = ni;
+  if (n_centers) *n_centers = nc;
+  return PKV_OK;
+}

@@ -1,0 +1,282 @@
+// Small kernels around the hot path:
+//   K4 pieces: window append + flush pattern refresh (engine.py:172-198,
+//              midrange_center patterns.py:161-171, PatternSet.append :51-60)
+//   K5 dequant: exact fp64 reconstruction (engine.py:255-303, quant.py:114-117)
+//   export:     fragment layout -> reference packed layout (engine.py:222,243)
+//   group API:  quantize_group / pack_codes / unpack_codes (quant.py:70-179),
+//               match_many (patterns.py:206-221), validation (engine.py:132-139)
+#include "pkv_common.cuh"
+
+namespace pkv {
+
+static inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ---- non-finite scan: first flat index of a non-finite element --------------------
+template <typename T>
+__global__ void finite_kernel(const T* x, int64_t n, unsigned long long* first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = to_f64(x[i]);
+    if (!isfinite(v)) atomicMin(first, (unsigned long long)i);
+  }
+}
+template <typename T>
+cudaError_t launch_finite(const T* x, int64_t n, unsigned long long* first, cudaStream_t st) {
+  int blocks = (int)imin64((n + 255) / 256, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  finite_kernel<T><<<blocks, 256, 0, st>>>(x, n, first);
+  return cudaGetLastError();
+}
+template cudaError_t launch_finite<__half>(const __half*, int64_t, unsigned long long*, cudaStream_t);
+template cudaError_t launch_finite<__nv_bfloat16>(const __nv_bfloat16*, int64_t, unsigned long long*, cudaStream_t);
+template cudaError_t launch_finite<float>(const float*, int64_t, unsigned long long*, cudaStream_t);
+template cudaError_t launch_finite<double>(const double*, int64_t, unsigned long long*, cudaStream_t);
+
+// ---- window ring: copy rows [U][nrows][D] into ring slots (slot0 + r) % Wcap -------
+template <typename T>
+__global__ void window_put_kernel(DevCache c, const T* k, const T* v, int64_t src_unit_stride, int nrows, int slot0) {
+  const int u = blockIdx.y;
+  const int64_t n = (int64_t)nrows * c.D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / c.D), ch = (int)(i - (int64_t)r * c.D);
+    const int64_t dst = ((int64_t)u * c.Wcap + (slot0 + r) % c.Wcap) * c.D + ch;
+    const int64_t src = (int64_t)u * src_unit_stride + i;
+    reinterpret_cast<T*>(c.wk)[dst] = k[src];
+    reinterpret_cast<T*>(c.wv)[dst] = v[src];
+  }
+}
+template <typename T>
+cudaError_t launch_window_put(const DevCache& c, const T* k, const T* v, int64_t sus, int nrows, int slot0, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  int gx = (int)imin64(((int64_t)nrows * c.D + 255) / 256, 64);
+  window_put_kernel<T><<<dim3(gx, c.U), 256, 0, st>>>(c, k, v, sus, nrows, slot0);
+  return cudaGetLastError();
+}
+template cudaError_t launch_window_put<__half>(const DevCache&, const __half*, const __half*, int64_t, int, int, cudaStream_t);
+template cudaError_t launch_window_put<__nv_bfloat16>(const DevCache&, const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int, int, cudaStream_t);
+template cudaError_t launch_window_put<float>(const DevCache&, const float*, const float*, int64_t, int, int, cudaStream_t);
+template cudaError_t launch_window_put<double>(const DevCache&, const double*, const double*, int64_t, int, int, cudaStream_t);
+
+// ---- flush refresh: midrange of the oldest G ring rows appended as a pattern -------
+// grid (U, 2 sides), block D threads.  0.5 * (min + max) in IEEE fp64.
+template <typename T>
+__global__ void refresh_kernel(DevCache c, int slot0, int G, int side_mask) {
+  const int u = blockIdx.x, side = blockIdx.y, ch = threadIdx.x;
+  if (!((side_mask >> side) & 1)) return;
+  const T* w = reinterpret_cast<const T*>(side == 0 ? c.wk : c.wv) + (int64_t)u * c.Wcap * c.D;
+  int* np_ = side == 0 ? c.nk : c.nv;
+  const int p = np_[u];
+  __shared__ float red[32];
+  float a = 0.f;
+  if (ch < c.D) {
+    double mn = 1.0 / 0.0, mx = -1.0 / 0.0;
+    for (int r = 0; r < G; ++r) {
+      double x = to_f64(w[(int64_t)((slot0 + r) % c.Wcap) * c.D + ch]);
+      mn = fmin(mn, x); mx = fmax(mx, x);
+    }
+    const double m = __dmul_rn(0.5, __dadd_rn(mn, mx));
+    (side == 0 ? c.kpat64 : c.vpat64)[((int64_t)u * c.Pcap + p) * c.D + ch] = m;
+    (side == 0 ? c.kpat32 : c.vpat32)[((int64_t)u * c.Pcap + p) * c.Dp + ch] = (float)m;
+    a = fabsf((float)m) * (1.f + 1e-6f);
+  }
+  for (int cc = c.D + ch; cc < c.Dp; cc += blockDim.x)
+    (side == 0 ? c.kpat32 : c.vpat32)[((int64_t)u * c.Pcap + p) * c.Dp + cc] = 0.f;
+  a = warp_max_f(a);
+  if ((ch & 31) == 0) red[ch >> 5] = a;
+  __syncthreads();
+  if (ch == 0) {
+    float m = 0.f;
+    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) m = fmaxf(m, red[i]);
+    float* pm = side == 0 ? c.kpmax : c.vpmax;
+    pm[u] = fmaxf(pm[u], m);
+    np_[u] = p + 1;
+  }
+}
+template <typename T>
+cudaError_t launch_refresh(const DevCache& c, int slot0, int G, int side_mask, cudaStream_t st) {
+  int threads = round_up(c.D, 32);
+  refresh_kernel<T><<<dim3(c.U, 2), threads, 0, st>>>(c, slot0, G, side_mask);
+  return cudaGetLastError();
+}
+template cudaError_t launch_refresh<__half>(const DevCache&, int, int, int, cudaStream_t);
+template cudaError_t launch_refresh<__nv_bfloat16>(const DevCache&, int, int, int, cudaStream_t);
+template cudaError_t launch_refresh<float>(const DevCache&, int, int, int, cudaStream_t);
+template cudaError_t launch_refresh<double>(const DevCache&, int, int, int, cudaStream_t);
+
+// ---- fragment-layout addressing (inverse of frag_rc) -------------------------------
+struct CodeLoc { int word; int shift; };
+__device__ __forceinline__ CodeLoc frag_locate(int row, int col16, int j, int bits, int WL) {
+  // row/col16 are the A-fragment coordinates inside sub-tile j
+  const int g = row & 7, hr = row >> 3, q = (col16 & 7) >> 1, hc = col16 >> 3, e = col16 & 1;
+  const int reg = hr + 2 * hc, lane = 4 * g + q, R = 4 * j + reg, S = 16 / bits;
+  CodeLoc l;
+  l.word = lane * WL + R / S;
+  l.shift = (e ? 16 : 0) + (R % S) * bits;
+  return l;
+}
+__device__ __forceinline__ int read_code(const uint8_t* blk, int side, int tok, int ch, int Dp, int bits) {
+  const int WL = frag_words_per_lane(Dp, bits);
+  const int tile = tok >> 4;
+  CodeLoc l = side == 0 ? frag_locate(tok & 15, ch & 15, ch >> 4, bits, WL) : frag_locate(ch & 15, tok & 15, ch >> 4, bits, WL);
+  const uint32_t w = reinterpret_cast<const uint32_t*>(blk + (size_t)tile * tile_bytes(Dp, bits))[l.word];
+  return (w >> l.shift) & ((1 << bits) - 1);
+}
+
+// block index of committed token t (blocks are contiguous in token order)
+__device__ __forceinline__ int find_block(const int64_t* start, int nb, int64_t t) {
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---- K5 exact dequant of committed tokens [t0, t1) -> fp64 [U][n][D] ----------------
+__global__ void dequant_kernel(DevCache c, int nb, int64_t t0, int64_t n, double* kout, double* vout) {
+  const int u = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * c.D; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + i / c.D;
+    const int ch = (int)(i % c.D);
+    const int b = find_block(c.blk_start, nb, t);
+    const int tb = (int)(t - c.blk_start[b]);
+    const uint8_t* kb = c.kcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
+    const uint8_t* vb = c.vcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
+    // K: scale_c * code + zero_c (+ pattern)   engine.py:255-261
+    const double* kp = c.kparam64 + ((int64_t)u * c.NBcap + b) * 2 * c.D;
+    double kv = __dadd_rn(__dmul_rn(kp[ch], (double)read_code(kb, 0, tb, ch, c.Dp, c.bits)), kp[c.D + ch]);
+    const int ki = c.kidx[(int64_t)u * c.Tcap + t];
+    if (ki >= 0) kv = __dadd_rn(kv, c.kpat64[((int64_t)u * c.Pcap + ki) * c.D + ch]);
+    // V: scale_t * code + zero_t (+ pattern)   engine.py:264-268
+    const double* vp = c.vparam64 + ((int64_t)u * c.Tcap + t) * 2;
+    double vv = __dadd_rn(__dmul_rn(vp[0], (double)read_code(vb, 1, tb, ch, c.Dp, c.bits)), vp[1]);
+    const int vi = c.vidx[(int64_t)u * c.Tcap + t];
+    if (vi >= 0) vv = __dadd_rn(vv, c.vpat64[((int64_t)u * c.Pcap + vi) * c.D + ch]);
+    kout[((int64_t)u * n + (i / c.D)) * c.D + ch] = kv;
+    vout[((int64_t)u * n + (i / c.D)) * c.D + ch] = vv;
+  }
+}
+cudaError_t launch_dequant(const DevCache& c, int nb, int64_t t0, int64_t n, double* k, double* v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int gx = (int)imin64((n * c.D + 255) / 256, 1024);
+  dequant_kernel<<<dim3(gx, c.U), 256, 0, st>>>(c, nb, t0, n, k, v);
+  return cudaGetLastError();
+}
+
+// ---- unpacked codes export: [U][n][D] uint8 for K and V (token-major) --------------
+__global__ void codes_kernel(DevCache c, int nb, int64_t t0, int64_t n, uint8_t* kc, uint8_t* vc) {
+  const int u = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * c.D; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + i / c.D;
+    const int ch = (int)(i % c.D);
+    const int b = find_block(c.blk_start, nb, t);
+    const int tb = (int)(t - c.blk_start[b]);
+    kc[(int64_t)u * n * c.D + i] = (uint8_t)read_code(c.kcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes, 0, tb, ch, c.Dp, c.bits);
+    vc[(int64_t)u * n * c.D + i] = (uint8_t)read_code(c.vcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes, 1, tb, ch, c.Dp, c.bits);
+  }
+}
+cudaError_t launch_codes(const DevCache& c, int nb, int64_t t0, int64_t n, uint8_t* k, uint8_t* v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int gx = (int)imin64((n * c.D + 255) / 256, 1024);
+  codes_kernel<<<dim3(gx, c.U), 256, 0, st>>>(c, nb, t0, n, k, v);
+  return cudaGetLastError();
+}
+
+// ---- group API ------------------------------------------------------------------------
+// quantize_group over many groups: values fp64 concatenated, offsets[n+1].
+// One warp per group (quant.py:70-111).
+__global__ void quantize_groups_kernel(const double* vals, const int64_t* offs, int ngroups, int bits,
+                                       double* scale, double* zero, uint8_t* codes) {
+  const int lane = threadIdx.x & 31;
+  const int gidx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (gidx >= ngroups) return;
+  const int64_t a = offs[gidx], b = offs[gidx + 1];
+  double lo = 1.0 / 0.0, hi = -1.0 / 0.0;
+  for (int64_t i = a + lane; i < b; i += 32) { lo = fmin(lo, vals[i]); hi = fmax(hi, vals[i]); }
+  lo = warp_min_d(lo); hi = warp_max_d(hi);
+  const QuantParamsDev qp = make_qparams(lo, hi, (1 << bits) - 1);
+  for (int64_t i = a + lane; i < b; i += 32) codes[i] = (uint8_t)quant_code(vals[i], qp, nullptr);
+  if (lane == 0) { scale[gidx] = qp.scale; zero[gidx] = qp.lo; }
+}
+cudaError_t launch_quantize_groups(const double* v, const int64_t* o, int n, int bits, double* s, double* z, uint8_t* c,
+                                   cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  quantize_groups_kernel<<<(n + 7) / 8, 256, 0, st>>>(v, o, n, bits, s, z, c);
+  return cudaGetLastError();
+}
+
+// pack: out byte i = OR_k codes[i*per + k] << (k*bits)   (quant.py:120-146)
+__global__ void pack_kernel(const uint8_t* codes, int64_t n, int bits, uint8_t* out) {
+  const int per = 8 / bits;
+  const int64_t nb = (n + per - 1) / per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned v = 0;
+    for (int k = 0; k < per; ++k) {
+      const int64_t j = i * per + k;
+      if (j < n) v |= (unsigned)codes[j] << (k * bits);
+    }
+    out[i] = (uint8_t)v;
+  }
+}
+__global__ void unpack_kernel(const uint8_t* in, int64_t n, int bits, uint8_t* codes) {
+  const int per = 8 / bits;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    codes[j] = (in[j / per] >> ((j % per) * bits)) & ((1 << bits) - 1);
+}
+cudaError_t launch_pack(const uint8_t* c, int64_t n, int bits, uint8_t* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int g = (int)imin64((n + 1023) / 1024, 1024);
+  pack_kernel<<<g, 256, 0, st>>>(c, n, bits, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack(const uint8_t* in, int64_t n, int bits, uint8_t* c, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int g = (int)imin64((n + 255) / 256, 1024);
+  unpack_kernel<<<g, 256, 0, st>>>(in, n, bits, c);
+  return cudaGetLastError();
+}
+
+// match_many in IEEE fp64 (patterns.py:206-221): one warp per vector, lane = pattern.
+__global__ void match_kernel(const double* x, int64_t n, const double* m, int P, int D, int64_t* idx, double* dist,
+                             double* res) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const double* xr = x + r * D;
+  double bestv = 1.0 / 0.0;
+  int besti = 0;
+  for (int pb = 0; pb < P; pb += 32) {
+    const int p = pb + lane;
+    double v = 1.0 / 0.0;
+    if (p < P) {
+      double mx = -1.0 / 0.0, mn = 1.0 / 0.0;
+      for (int c = 0; c < D; ++c) { double d = __dsub_rn(xr[c], m[(int64_t)p * D + c]); mx = fmax(mx, d); mn = fmin(mn, d); }
+      v = __dsub_rn(mx, mn);
+    }
+    int pi = p;
+    warp_argmin_d(v, pi);
+    if (v < bestv) { bestv = v; besti = pi; }
+  }
+  if (lane == 0) { idx[r] = besti; dist[r] = bestv; }
+  for (int c = lane; c < D; c += 32) res[r * D + c] = __dsub_rn(xr[c], m[(int64_t)besti * D + c]);
+}
+cudaError_t launch_match(const double* x, int64_t n, const double* m, int P, int D, int64_t* idx, double* dist, double* res,
+                         cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  match_kernel<<<(int)((n + 7) / 8), 256, 0, st>>>(x, n, m, P, D, idx, dist, res);
+  return cudaGetLastError();
+}
+
+// midrange over rows (patterns.py:161-171)
+__global__ void midrange_kernel(const double* x, int64_t n, int D, double* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= D) return;
+  double mn = 1.0 / 0.0, mx = -1.0 / 0.0;
+  for (int64_t r = 0; r < n; ++r) { double v = x[r * D + c]; mn = fmin(mn, v); mx = fmax(mx, v); }
+  out[c] = __dmul_rn(0.5, __dadd_rn(mn, mx));
+}
+cudaError_t launch_midrange(const double* x, int64_t n, int D, double* out, cudaStream_t st) {
+  midrange_kernel<<<(D + 127) / 128, 128, 0, st>>>(x, n, D, out);
+  return cudaGetLastError();
+}
+
+}  // namespace pkv
