@@ -43,6 +43,7 @@ extern "C" {
 /* cache flags */
 #define PKV_FLAG_DECISIONS 1 /* keep per-token gate ranges (GateDecision records) */
 #define PKV_FLAG_STATS 2     /* count fp64 refinements / exact-division fallbacks */
+#define PKV_FLAG_BRUTE_FORCE 4 /* exhaustive d_mm matching (disable lower-bound pruning) */
 
 /* EngineConfig, field for field (engine.py:38-83) */
 typedef struct pkv_config {

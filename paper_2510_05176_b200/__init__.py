@@ -1,16 +1,58 @@
 """B200-native PatternKV codec (arXiv 2510.05176): pattern-aligned residual
-KV-cache quantization with hand-written sm_100a kernels behind a C ABI.
+KV-cache quantization with hand-written sm_100a kernels behind a C ABI
+(include/pkv.h, libpkv_b200.so).
 
-Production API: ``PatternKVCache`` (batched units on one GPU).
-Drop-in API: the reference package's names (``prefill``,
-``append_decode_token``, ``quantize_group``, ...) re-exported below with the
-reference's signatures, argument meaning and error behaviour.
+Production API: ``PatternKVCache`` -- U independent (batch, layer, kv-head)
+units on one GPU: prefill (mine + encode), append-and-refresh, decode
+attention over the compressed cache, exact dequant.
+Drop-in API: the reference package's hot-path names (pkg/src/patternkv/
+__init__.py:10-94) with the reference's signatures, argument meaning and
+error behaviour, executed on the GPU.
 """
 
-from .errors import DataError, UsageError
 from . import _lib  # noqa: F401  (fails loudly when libpkv_b200.so is missing)
-from .cache import RAW_MARKER, PatternKVCache, first_seed_index
+from .analysis import KvStream, bits_per_token, fp16_reference_bits_per_token
+from .cache import PatternKVCache, first_seed_index
+from .config import EngineConfig
+from .engine import (
+    RAW_MARKER,
+    CacheMetrics,
+    CommittedKBlock,
+    CommittedVToken,
+    HeadCacheState,
+    HeadReport,
+    accounted_bits_per_token,
+    append_decode_token,
+    committed_matrices,
+    prefill,
+    reconstruct_token,
+    replay_head,
+    run_scheme_comparison,
+)
+from .errors import DataError, UsageError
+from .gate import GateConfig, GateDecision, contraction_threshold, decide, expected_error_gain, z_quantile
+from .patterns import (
+    PatternMatch,
+    PatternSet,
+    lloyd_kmeans,
+    match_many,
+    match_pattern,
+    midrange_center,
+    mine_patterns,
+    minmax_distance,
+    reconstruct_vector,
+)
+from .quant import QuantizedGroup, QuantParams, dequantize_group, pack_codes, quantize_group, unpack_codes
 
 __version__ = "0.1.0"
 
-__all__ = ["DataError", "UsageError", "PatternKVCache", "RAW_MARKER", "first_seed_index"]
+__all__ = [
+    "PatternKVCache", "first_seed_index", "KvStream", "bits_per_token", "fp16_reference_bits_per_token",
+    "EngineConfig", "RAW_MARKER", "CacheMetrics", "CommittedKBlock", "CommittedVToken", "HeadCacheState",
+    "HeadReport", "accounted_bits_per_token", "append_decode_token", "committed_matrices", "prefill",
+    "reconstruct_token", "replay_head", "run_scheme_comparison", "DataError", "UsageError", "GateConfig",
+    "GateDecision", "contraction_threshold", "decide", "expected_error_gain", "z_quantile", "PatternMatch",
+    "PatternSet", "lloyd_kmeans", "match_many", "match_pattern", "midrange_center", "mine_patterns",
+    "minmax_distance", "reconstruct_vector", "QuantizedGroup", "QuantParams", "dequantize_group", "pack_codes",
+    "quantize_group", "unpack_codes",
+]

@@ -21,7 +21,6 @@ namespace pkv {
 constexpr int ATT_WARPS = 4;
 constexpr int ATT_THREADS = ATT_WARPS * 32;
 constexpr int MAXG = 8;         // GQA group size served (query heads per KV head)
-constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_TH = 8.f;  // lazy rescale threshold (log2 units)
 
 __device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
@@ -76,6 +75,40 @@ __device__ __forceinline__ void load_words(const uint8_t* tile, int lane, uint32
   }
 }
 
+constexpr int ATT_STAGES = 4;
+
+// per-lane private pattern-weight copies while they fit in 64 KB
+__host__ __device__ inline bool attn_w_private(int Pv, int NT) {
+  return (size_t)ATT_WARPS * 8 * (Pv > 1 ? Pv : 1) * 4 * NT * 4 <= 64 * 1024;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int BITS>
+__device__ __forceinline__ void load_stage_words(const unsigned char* p, uint32_t* w, int WL) {
+  constexpr int NW = 16 * BITS / 8;  // words per lane at Dp = 128
+  if (WL == NW) {
+#pragma unroll
+    for (int i = 0; i < NW / 4; ++i) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[i];
+      w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) w[i] = i < WL ? reinterpret_cast<const uint32_t*>(p)[i] : 0u;
+  }
+}
+
 // A fragments of sub-tile j (4 half2 registers) from the lane's code words.
 template <int BITS>
 __device__ __forceinline__ void afrag(const uint32_t* w, int j, uint32_t* a) {
@@ -87,22 +120,29 @@ __device__ __forceinline__ void afrag(const uint32_t* w, int j, uint32_t* a) {
   }
 }
 
-template <int BITS, int NT>
+template <int BITS, int NT, int KT>
 __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kernel(DevCache c, AttnArgs a) {
   const int u = blockIdx.y, chunk = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, qd = lane & 3;
-  const int Dp = c.Dp, D = c.D, G = a.G;
-  const int KT = Dp / 16;
-  const int WL = frag_words_per_lane(Dp, BITS);
+  constexpr int Dp = 16 * KT;  // == c.Dp
+  constexpr int WL = Dp * BITS / 64;
+  const int D = c.D, G = a.G;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* sq = reinterpret_cast<float*>(smem_raw);                 // [MAXG][Dp]
   float* sqm = sq + MAXG * Dp;                                     // [Pk][MAXG]
   const int Pk = c.use_kp ? c.nk[u] : 0;
   const int Pv = c.use_vp ? c.nv[u] : 0;
-  float* sW = sqm + (size_t)max(Pk, 1) * MAXG;                     // [warps][Pv][MAXG]
-  __half* sP = reinterpret_cast<__half*>(sW + (size_t)ATT_WARPS * max(Pv, 1) * MAXG);  // [warps][16][16]
+  // pattern weights W_p = sum_{t: idx_t = p} p_t.  priv: one private copy per lane
+  // ([warps][g][Pv][HN], plain read-modify-write, no atomics); else shared per warp
+  // ([warps][Pv][MAXG]) with atomics.  Wc = the merged [Pv][MAXG] table.
+  constexpr int HN = 4 * NT;
+  const bool priv = attn_w_private(Pv, NT);
+  const size_t wfl = priv ? (size_t)ATT_WARPS * 8 * max(Pv, 1) * HN : (size_t)ATT_WARPS * max(Pv, 1) * MAXG;
+  float* sW = sqm + (size_t)max(Pk, 1) * MAXG;
+  float* Wc = sW + wfl;                                             // [Pv][MAXG]
+  __half* sP = reinterpret_cast<__half*>(Wc + (size_t)max(Pv, 1) * MAXG);  // [warps][16][16]
   float* sred = reinterpret_cast<float*>(sP + ATT_WARPS * 256);   // [warps][MAXG][4]
 
   // ---- per-unit setup: q, q.M table, zeroed pattern weights -----------------------
@@ -110,7 +150,7 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
     const int h = i / Dp, ch = i - h * Dp;
     sq[i] = (h < G && ch < D) ? a.q[((int64_t)u * G + h) * D + ch] : 0.f;
   }
-  for (int i = tid; i < ATT_WARPS * max(Pv, 1) * MAXG; i += ATT_THREADS) sW[i] = 0.f;
+  for (size_t i = tid; i < wfl; i += ATT_THREADS) sW[i] = 0.f;
   __syncthreads();
   for (int i = tid; i < Pk * MAXG; i += ATT_THREADS) {
     const int p = i / MAXG, h = i - p * MAXG;
@@ -135,18 +175,64 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
   float mrun[NT], lsum[NT], zsum[NT];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) { mrun[nt] = -INFINITY; lsum[nt] = 0.f; zsum[nt] = 0.f; }
-  float* myW = sW + (size_t)warp * max(Pv, 1) * MAXG;
+  // this lane's W slot for (pattern p, head 4nt+qd)
+  auto wslot = [&](int p, int nt) -> float* {
+    return priv ? sW + (((size_t)warp * 8 + g) * max(Pv, 1) + p) * HN + 4 * nt + qd
+                : sW + ((size_t)warp * max(Pv, 1) + p) * MAXG + 4 * nt + qd;
+  };
   __half* myP = sP + warp * 256;
 
   const int b0 = chunk * a.bpc;
   const int b1 = min(a.nb, b0 + a.bpc);
+  // ---- cp.async pipeline over this warp's (block, tile) items -----------------------
+  // stage = K codes tile | V codes tile | kidx[16] | vidx[16] | vparam[16][2]
+  constexpr int KCB = WL * 4;                   // code bytes per lane per tile
+  constexpr int SB = (2 * 32 * KCB + 192 + 15) / 16 * 16;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(sred + ATT_WARPS * MAXG * 4) + (size_t)warp * ATT_STAGES * SB;
+  constexpr int tbytes = 16 * Dp * BITS / 8;
+  int pb = b0 + warp, pti = 0;                  // producer cursor
+  int pnt = pb < b1 ? (c.blk_len[pb] + 15) >> 4 : 0;
+  auto issue = [&](int stage) {
+    unsigned char* st = ring + stage * SB;
+    if (pb < b1) {
+      const int64_t bo = (int64_t)u * c.NBcap + pb;
+      const uint8_t* ksrc = c.kcodes + bo * c.blk_bytes + pti * tbytes + lane * KCB;
+      const uint8_t* vsrc = c.vcodes + bo * c.blk_bytes + pti * tbytes + lane * KCB;
+      if ((KCB & 15) == 0) {
+        for (int o = 0; o < KCB; o += 16) {
+          cp_async16(st + lane * KCB + o, ksrc + o);
+          cp_async16(st + 32 * KCB + lane * KCB + o, vsrc + o);
+        }
+      } else {
+        for (int o = 0; o < KCB; o += 4) {
+          cp_async4(st + lane * KCB + o, ksrc + o);
+          cp_async4(st + 32 * KCB + lane * KCB + o, vsrc + o);
+        }
+      }
+      const int64_t slot = bo * c.GP + pti * 16;
+      unsigned char* meta = st + 64 * KCB;
+      if (lane < 2) cp_async16(meta + 16 * lane, reinterpret_cast<const uint8_t*>(c.kidx + slot) + 16 * lane);
+      else if (lane < 4) cp_async16(meta + 32 + 16 * (lane - 2), reinterpret_cast<const uint8_t*>(c.vidx + slot) + 16 * (lane - 2));
+      else if (lane < 12) cp_async16(meta + 64 + 16 * (lane - 4), reinterpret_cast<const uint8_t*>(c.vparam32 + 2 * slot) + 16 * (lane - 4));
+      if (++pti == pnt) {
+        pti = 0;
+        pb += ATT_WARPS;
+        pnt = pb < b1 ? (c.blk_len[pb] + 15) >> 4 : 0;
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < ATT_STAGES - 1; ++s) issue(s);
+
+  uint32_t bq[8][NT][2];
+  float qz[NT];
+  int L = 0;
+  int stage = 0;
   for (int b = b0 + warp; b < b1; b += ATT_WARPS) {
-    const int L = c.blk_len[b];
-    const int64_t tstart = c.blk_start[b];
+    L = c.blk_len[b];
     const float* kp = c.kparam32 + ((int64_t)u * c.NBcap + b) * 2 * Dp;
     // B fragments of q o s_b (hi/lo columns) and q.z_b per head
-    uint32_t bq[8][NT][2];
-    float qz[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int col = 8 * nt + g, h = col >> 1, hl = col & 1;
@@ -157,9 +243,9 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int ch = 16 * kt + 2 * qd + 8 * hh;
-            const float2 s2 = *reinterpret_cast<const float2*>(kp + ch);
-            const float2 z2 = *reinterpret_cast<const float2*>(kp + Dp + ch);
-            const float q0 = h < MAXG ? sq[h * Dp + ch] : 0.f, q1 = h < MAXG ? sq[h * Dp + ch + 1] : 0.f;
+            const float2 s2 = __ldg(reinterpret_cast<const float2*>(kp + ch));
+            const float2 z2 = __ldg(reinterpret_cast<const float2*>(kp + Dp + ch));
+            const float q0 = sq[h * Dp + ch], q1 = sq[h * Dp + ch + 1];
             const float t0 = q0 * s2.x, t1 = q1 * s2.y;
             const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
             __half e0 = h0, e1 = h1;
@@ -173,23 +259,26 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       zpart += __shfl_xor_sync(0xffffffffu, zpart, 2);
       qz[nt] = __shfl_sync(0xffffffffu, zpart, 8 * qd);  // head 4nt+qd lives at g = 2qd
     }
-
-    const uint8_t* kblk = c.kcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
-    const uint8_t* vblk = c.vcodes + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
     const int ntile = (L + 15) >> 4;
     for (int ti = 0; ti < ntile; ++ti) {
-      const int tbytes = tile_bytes(Dp, BITS);
+      cp_async_wait<ATT_STAGES - 2>();
+      __syncwarp();
+      const unsigned char* st = ring + stage * SB;
       uint32_t kw[16 * BITS / 8], vw[16 * BITS / 8];
-      load_words<BITS>(kblk + ti * tbytes, lane, kw, WL);
-      load_words<BITS>(vblk + ti * tbytes, lane, vw, WL);
-      // token metadata for rows g, g+8
+      load_stage_words<BITS>(st + lane * KCB, kw, WL);
+      load_stage_words<BITS>(st + 32 * KCB + lane * KCB, vw, WL);
+      const int16_t* mk = reinterpret_cast<const int16_t*>(st + 64 * KCB);
+      const int16_t* mv = mk + 16;
+      const float2* mp = reinterpret_cast<const float2*>(st + 64 * KCB + 64);
       const int r0 = 16 * ti + g, r1 = r0 + 8;
       const bool ok0 = r0 < L, ok1 = r1 < L;
-      const int64_t tk0 = (int64_t)u * c.Tcap + tstart + r0, tk1 = tk0 + 8;
-      const int ki0 = ok0 ? c.kidx[tk0] : -1, ki1 = ok1 ? c.kidx[tk1] : -1;
-      const int vi0 = ok0 ? c.vidx[tk0] : -1, vi1 = ok1 ? c.vidx[tk1] : -1;
-      const float2 vp0 = ok0 ? *reinterpret_cast<const float2*>(c.vparam32 + 2 * tk0) : make_float2(0.f, 0.f);
-      const float2 vp1 = ok1 ? *reinterpret_cast<const float2*>(c.vparam32 + 2 * tk1) : make_float2(0.f, 0.f);
+      const int ki0 = ok0 ? mk[g] : -1, ki1 = ok1 ? mk[g + 8] : -1;
+      const int vi0 = ok0 ? mv[g] : -1, vi1 = ok1 ? mv[g + 8] : -1;
+      const float2 vp0 = ok0 ? mp[g] : make_float2(0.f, 0.f);
+      const float2 vp1 = ok1 ? mp[g + 8] : make_float2(0.f, 0.f);
+      __syncwarp();
+      issue((stage + ATT_STAGES - 1) % ATT_STAGES);  // refill the slot consumed last iteration
+      stage = (stage + 1) % ATT_STAGES;
 
       // ---- S = K . (q o s): tokens on M, hi/lo head columns on N ----
       float sacc[NT][4];
@@ -227,17 +316,23 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
           for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) oacc[mt][nt][r] *= alpha;
-          if (h < MAXG)
-            for (int p = g; p < Pv; p += 8) myW[p * MAXG + h] *= alpha;
+          if (priv) {
+            for (int p = 0; p < Pv; ++p) *wslot(p, nt) *= alpha;
+          } else {
+            for (int p = g; p < Pv; p += 8) *wslot(p, nt) *= alpha;
+          }
           mrun[nt] = mnew;
         }
         const float p0 = exp2f(s0 - mrun[nt]), p1 = exp2f(s1 - mrun[nt]);
         lsum[nt] += p0 + p1;
         zsum[nt] = fmaf(p0, vp0.y, fmaf(p1, vp1.y, zsum[nt]));
-        __syncwarp();  // rescaled W visible before other lanes add into it
-        if (h < MAXG) {
-          if (vi0 >= 0 && p0 != 0.f) atomicAdd(&myW[vi0 * MAXG + h], p0);
-          if (vi1 >= 0 && p1 != 0.f) atomicAdd(&myW[vi1 * MAXG + h], p1);
+        if (priv) {
+          if (vi0 >= 0) *wslot(vi0, nt) += p0;
+          if (vi1 >= 0) *wslot(vi1, nt) += p1;
+        } else {
+          __syncwarp();  // rescaled W visible before other lanes add into it
+          if (vi0 >= 0 && p0 != 0.f) atomicAdd(wslot(vi0, nt), p0);
+          if (vi1 >= 0 && p1 != 0.f) atomicAdd(wslot(vi1, nt), p1);
         }
         const float w0 = p0 * vp0.x, w1 = p1 * vp1.x;
         const __half w0h = __float2half_rn(w0), w1h = __float2half_rn(w1);
@@ -266,6 +361,7 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       }
     }
   }
+  cp_async_wait<0>();
 
   // ---- merge the warps of the CTA --------------------------------------------------
   // per-head running max m (same for the 8 lanes of a head), l and z partial per lane
@@ -308,14 +404,25 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       }
     }
   }
-  // pattern weights: W = sum_w fac_w W_w  (lanes of head h hold fac for their warp)
-  if (Pv > 0) {
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int h = 4 * nt + qd;
-      if (h < MAXG)
-        for (int p = g; p < Pv; p += 8) myW[p * MAXG + h] *= fac[nt];
+  __syncthreads();
+  // pattern weights merged over warps (and private lane copies): Wc[p][h] = sum_w fac_w(h) W_w[p][h]
+  for (int i = tid; i < Pv * HN; i += ATT_THREADS) {
+    const int p = i / HN, h = i - p * HN;
+    float M = -INFINITY;
+    for (int w = 0; w < ATT_WARPS; ++w) M = fmaxf(M, sred[(w * MAXG + h) * 4]);
+    float acc = 0.f;
+    for (int w = 0; w < ATT_WARPS; ++w) {
+      const float mw = sred[(w * MAXG + h) * 4];
+      if (mw == -INFINITY) continue;
+      float sw = 0.f;
+      if (priv) {
+        for (int gg = 0; gg < 8; ++gg) sw += sW[(((size_t)w * 8 + gg) * Pv + p) * HN + h];
+      } else {
+        sw = sW[((size_t)w * Pv + p) * MAXG + h];
+      }
+      acc = fmaf(exp2f(mw - M), sw, acc);
     }
+    Wc[p * MAXG + h] = acc;
   }
   __syncthreads();
   // final per-head sums and the pattern / zero-point terms, then write the partial
@@ -330,11 +437,7 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
     }
     float o = sq[i] + zt;
     if (ch < D) {
-      for (int p = 0; p < Pv; ++p) {
-        float wsum = 0.f;
-        for (int w = 0; w < ATT_WARPS; ++w) wsum += sW[((size_t)w * max(Pv, 1) + p) * MAXG + h];
-        o = fmaf(wsum, c.vpat32[((int64_t)u * c.Pcap + p) * Dp + ch], o);
-      }
+      for (int p = 0; p < Pv; ++p) o = fmaf(Wc[p * MAXG + h], c.vpat32[((int64_t)u * c.Pcap + p) * Dp + ch], o);
     }
     out[h * (Dp + 2) + ch] = o;
     if (ch == 0) {
@@ -395,16 +498,28 @@ __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_s
   for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) dst[lane + 32 * j] = o[j] * inv;
 }
 
-size_t attn_smem_bytes(int Dp, int Pk, int Pv) {
-  return (size_t)MAXG * Dp * 4 + (size_t)max(Pk, 1) * MAXG * 4 + (size_t)ATT_WARPS * max(Pv, 1) * MAXG * 4 +
-         ATT_WARPS * 256 * 2 + ATT_WARPS * MAXG * 4 * 4;
+size_t attn_smem_bytes(int Dp, int Pk, int Pv, int bits, int NT) {
+  const int SB = round_up(2 * 32 * frag_words_per_lane(Dp, bits) * 4 + 192, 16);
+  const size_t wfl = attn_w_private(Pv, NT) ? (size_t)ATT_WARPS * 8 * max(Pv, 1) * 4 * NT
+                                             : (size_t)ATT_WARPS * max(Pv, 1) * MAXG;
+  return (size_t)MAXG * Dp * 4 + (size_t)max(Pk, 1) * MAXG * 4 + wfl * 4 + (size_t)max(Pv, 1) * MAXG * 4 +
+         ATT_WARPS * 256 * 2 + ATT_WARPS * MAXG * 4 * 4 + (size_t)ATT_WARPS * ATT_STAGES * SB + 16;
 }
 
+template <int BITS, int NT, int KT>
+static cudaError_t launch_chunks_kt(const DevCache& c, const AttnArgs& a, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(attn_chunk_kernel<BITS, NT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  attn_chunk_kernel<BITS, NT, KT><<<dim3(a.nchunk, c.U), ATT_THREADS, smem, st>>>(c, a);
+  return cudaGetLastError();
+}
 template <int BITS, int NT>
 static cudaError_t launch_chunks(const DevCache& c, const AttnArgs& a, size_t smem, cudaStream_t st) {
-  cudaFuncSetAttribute(attn_chunk_kernel<BITS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  attn_chunk_kernel<BITS, NT><<<dim3(a.nchunk, c.U), ATT_THREADS, smem, st>>>(c, a);
-  return cudaGetLastError();
+  switch (c.Dp / 16) {
+    case 2: return launch_chunks_kt<BITS, NT, 2>(c, a, smem, st);
+    case 4: return launch_chunks_kt<BITS, NT, 4>(c, a, smem, st);
+    case 6: return launch_chunks_kt<BITS, NT, 6>(c, a, smem, st);
+    default: return launch_chunks_kt<BITS, NT, 8>(c, a, smem, st);
+  }
 }
 
 template <typename T>
@@ -412,8 +527,8 @@ cudaError_t launch_attn(const DevCache& c, const AttnArgs& a, int Pk_max, int Pv
                         float* out, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   if (a.nb > 0) {
-    size_t smem = attn_smem_bytes(c.Dp, Pk_max, Pv_max);
     const int nt = a.G <= 4 ? 1 : 2;
+    size_t smem = attn_smem_bytes(c.Dp, Pk_max, Pv_max, c.bits, nt);
     if (c.bits == 2) e = nt == 1 ? launch_chunks<2, 1>(c, a, smem, st) : launch_chunks<2, 2>(c, a, smem, st);
     else if (c.bits == 4) e = nt == 1 ? launch_chunks<4, 1>(c, a, smem, st) : launch_chunks<4, 2>(c, a, smem, st);
     else e = nt == 1 ? launch_chunks<8, 1>(c, a, smem, st) : launch_chunks<8, 2>(c, a, smem, st);

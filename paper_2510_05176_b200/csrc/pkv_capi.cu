@@ -212,9 +212,6 @@ static int reserve(pkv_cache* c, int64_t Tcap, int Pcap, cudaStream_t st) {
   if (Tcap > d.Tcap) {
     const int64_t oT = d.Tcap, oNB = d.NBcap;
     const int64_t nNB = nb_cap_for(Tcap, d.G);
-    CU(regrow(&d.kidx, U, oT, Tcap, 2, st));
-    CU(regrow(&d.vidx, U, oT, Tcap, 2, st));
-    CU(regrow(&d.vparam32, U, oT, Tcap, 8, st));
     CU(regrow(&d.vparam64, U, oT, Tcap, 16, st));
     if (d.keep_diag) {
       CU(regrow(&d.kdiag, U, oT, Tcap, 16, st));
@@ -224,6 +221,9 @@ static int reserve(pkv_cache* c, int64_t Tcap, int Pcap, cudaStream_t st) {
     CU(regrow(&d.vcodes, U, oNB, nNB, (size_t)d.blk_bytes, st));
     CU(regrow(&d.kparam32, U, oNB, nNB, (size_t)2 * Dp * 4, st));
     CU(regrow(&d.kparam64, U, oNB, nNB, (size_t)2 * D * 8, st));
+    CU(regrow(&d.kidx, U, oNB, nNB, (size_t)d.GP * 2, st));
+    CU(regrow(&d.vidx, U, oNB, nNB, (size_t)d.GP * 2, st));
+    CU(regrow(&d.vparam32, U, oNB, nNB, (size_t)d.GP * 8, st));
     CU(regrow(&d.blk_start, 1, oNB, nNB, 8, st));
     CU(regrow(&d.blk_len, 1, oNB, nNB, 4, st));
     d.Tcap = Tcap;
@@ -266,11 +266,13 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
   d.U = n_units; d.D = head_dim; d.Dp = c->Dp; d.bits = cfg->bits; d.qmax = (1 << cfg->bits) - 1;
   d.G = cfg->group_size; d.W = cfg->residual_window; d.Wcap = cfg->residual_window + cfg->group_size;
   d.ntile_blk = (cfg->group_size + 15) / 16;
+  d.GP = 16 * d.ntile_blk;
   d.blk_bytes = d.ntile_blk * tile_bytes(c->Dp, cfg->bits);
   d.in_dtype = in_dtype;
   d.use_kp = cfg->use_k_patterns; d.use_vp = cfg->use_v_patterns; d.use_vgate = cfg->use_v_gate;
   d.use_kgate = cfg->use_k_gate; d.gen_new = cfg->generate_new_patterns;
   d.keep_diag = (flags & PKV_FLAG_DECISIONS) ? 1 : 0;
+  d.prune = (flags & PKV_FLAG_BRUTE_FORCE) ? 0 : 1;
   d.thr = thr;
   cudaStream_t st = 0;
   auto bail = [&](int code) { pkv_cache_destroy(c); return code; };
@@ -346,12 +348,12 @@ extern "C" int pkv_cache_buffer(pkv_cache* c, const char* name, void** ptr, int6
   struct { const char* n; void* p; int64_t b; } tab[] = {
       {"kpat64", d.kpat64, U * P * D * 8}, {"vpat64", d.vpat64, U * P * D * 8},
       {"kparam64", d.kparam64, U * NB * 2 * D * 8}, {"vparam64", d.vparam64, U * T * 16},
-      {"kidx", d.kidx, U * T * 2}, {"vidx", d.vidx, U * T * 2},
+      {"kidx", d.kidx, U * NB * d.GP * 2}, {"vidx", d.vidx, U * NB * d.GP * 2},
       {"kdiag", d.kdiag, d.keep_diag ? U * T * 16 : 0}, {"vdiag", d.vdiag, d.keep_diag ? U * T * 16 : 0},
       {"wk", d.wk, U * d.Wcap * D * c->esize}, {"wv", d.wv, U * d.Wcap * D * c->esize},
       {"nk", d.nk, U * 4}, {"nv", d.nv, U * 4}, {"blk_start", d.blk_start, NB * 8}, {"blk_len", d.blk_len, NB * 4},
       {"kcodes", d.kcodes, U * NB * d.blk_bytes}, {"vcodes", d.vcodes, U * NB * d.blk_bytes},
-      {"kparam32", d.kparam32, U * NB * 2 * d.Dp * 4}, {"vparam32", d.vparam32, U * T * 8},
+      {"kparam32", d.kparam32, U * NB * 2 * d.Dp * 4}, {"vparam32", d.vparam32, U * NB * d.GP * 8},
       {"kpat32", d.kpat32, U * P * d.Dp * 4}, {"vpat32", d.vpat32, U * P * d.Dp * 4},
   };
   for (auto& e : tab) {

@@ -5,10 +5,11 @@
 //              kpat32/vpat32 [U][Pcap][Dp] f32 (fast-filter copies, pad = 0)
 //   K blocks   kcodes  [U][NBcap][blk_bytes]  mma-fragment order (see frag_pos)
 //              kparam32[U][NBcap][2][Dp] f32 (scale, zero)  kparam64 [U][NBcap][2][D] f64
-//              kidx    [U][Tcap] int16 (RAW = -1), indexed by committed token
+//              kidx    [U][NBcap][GP] int16 (RAW = -1), block-slot order (GP = 16*ntiles)
 //   V tokens   vcodes  [U][NBcap][blk_bytes]  mma-fragment order (V^T operand)
-//              vparam32[U][Tcap][2] f32        vparam64 [U][Tcap][2] f64
-//              vidx    [U][Tcap] int16
+//              vparam32[U][NBcap][GP][2] f32   vparam64 [U][Tcap][2] f64 (by token)
+//              vidx    [U][NBcap][GP] int16   (per-token decode metadata in block slots,
+//                                             so every tile's metadata is 16B aligned)
 //   window     wk/wv   [U][Wcap][D] in the input dtype, ring of W+G rows
 //
 // A block is one K quantization group span (<= G <= 128 tokens), stored as
@@ -151,9 +152,11 @@ __host__ __device__ inline int tile_bytes(int Dp, int bits) { return 16 * Dp * b
 // ---- device view of a cache -------------------------------------------------------
 struct DevCache {
   int U, D, Dp, bits, qmax, G, W, Wcap, ntile_blk, blk_bytes, in_dtype;
+  int GP;                          // token slots per block (16 * ntile_blk)
   int64_t Tcap, NBcap;
   int Pcap;
   int use_kp, use_vp, use_vgate, use_kgate, gen_new, keep_diag;
+  int prune;                      // K1 lower-bound pruned matcher (exact; 0 = brute force)
   double thr;
   // patterns
   double* kpat64; double* vpat64;

@@ -23,17 +23,25 @@ struct EncSmem {
   int DS, Dm;
   float* xs;      // [GMAX][DS] span rows (fp32; exact for 16/32-bit inputs)
   float* ms;      // [32][DS] pattern chunk
-  uint8_t* codes; // [GMAX][Dp] code tile
+  uint8_t* codes; // [GMAX][CS] code tile (CS = Dp + 4: conflict-free row writes)
+  int CS;
   float* xabs;    // [GMAX]
   float* best1; float* best2; int* bidx; int* fidx;  // [GMAX]
   double* qlo; double* qhi;  // [2][DMAX]
+  int* probe;     // [NPROBE] probe channels (pruned matcher)
+  float* mpk;     // [NPROBE][64] pattern values at the probe channels
 };
+
+constexpr int NPROBE = 16;   // channels of the d_mm lower bound
+constexpr int PRUNE_PMAX = 64;
+constexpr int PRUNE_MAXCAND = 6;
 
 __host__ __device__ inline size_t enc_smem_bytes(int D, int Dp) {
   int Dm = round_up(D, 4), DS = Dm + 4;
-  size_t b = (size_t)(GMAX + 32) * DS * 4 + (size_t)GMAX * Dp + 4 * GMAX * 4 + 2 * GMAX * 4;
+  size_t b = (size_t)(GMAX + 32) * DS * 4 + (size_t)GMAX * (Dp + 4) + 4 * GMAX * 4 + 2 * GMAX * 4;
   b = (b + 15) / 16 * 16;
   b += 4 * DMAX * 8;
+  b += NPROBE * 4 + NPROBE * PRUNE_PMAX * 4;
   return b;
 }
 
@@ -49,7 +57,9 @@ __device__ __forceinline__ void top2_merge(float& a1, int& ai, float& a2, float 
 
 template <typename T>
 __device__ __forceinline__ const T* span_row(const SpanSrc<T>& s, int u, int64_t off, int r, int D) {
-  return s.base + (int64_t)u * s.unit_stride + ((s.row0 + off + r) % s.ring) * (int64_t)D;
+  int64_t rr = s.row0 + off + r;
+  if (rr >= s.ring) rr = rr < 2 * s.ring ? rr - s.ring : rr % s.ring;  // window ring wrap (rare, small)
+  return s.base + (int64_t)u * s.unit_stride + rr * (int64_t)D;
 }
 
 template <typename T>
@@ -83,9 +93,391 @@ __device__ int refine_match64(const EncSmem& sm, const T* row, int r, const doub
   return besti;
 }
 
+constexpr float TWO_M22 = 2.384185791015625e-07f;  // 2^-22
+constexpr float TWO_M21 = 4.76837158203125e-07f;   // 2^-21
+constexpr float TWO_M20 = 9.5367431640625e-07f;    // 2^-20
+
+// fp32 fast path quantizer for inputs exact in fp32: t = (v32 - lo32)/scale + 1/2
+// with a per-group guard covering |v32 - v64| <= 2^-23 * S (S bounds |x|+|m|)
+// plus the fp32 rounding of the quotient; a code whose fraction lands inside
+// the guard is recomputed in fp64 from the exact payload.
+struct FastQ {
+  QuantParamsDev qp;
+  float lo32, guard;
+};
+__device__ __forceinline__ FastQ make_fastq(double lo, double hi, int qmax, float S) {
+  FastQ f;
+  f.qp = make_qparams(lo, hi, qmax);
+  f.lo32 = (float)lo;
+  if (f.qp.scale == 0.0) { f.guard = 0.f; return f; }
+  const float span = (float)(hi - lo);
+  const float g = TWO_M21 * (S + fabsf(f.lo32) + span) * f.qp.inv32 + TWO_M20 * (float)(qmax + 1);
+  f.guard = fminf(g, 0.5f);
+  return f;
+}
+template <typename ExactFn>
+__device__ __forceinline__ int fast_code(float v32, const FastQ& f, ExactFn exact64, unsigned* n_exact) {
+  if (f.qp.scale == 0.0) return 0;
+  const float t = __fmaf_rn(v32 - f.lo32, f.qp.inv32, 0.5f);
+  const float fl = floorf(t);
+  const float fr = t - fl;
+  int cde;
+  if (fr > f.guard && fr < 1.f - f.guard) {
+    cde = (int)fl;
+  } else {
+    const double q = __dadd_rn(__ddiv_rn(__dsub_rn(exact64(), f.qp.lo), f.qp.scale), 0.5);
+    cde = (int)floor(q);
+    if (n_exact) atomicAdd(n_exact, 1u);
+  }
+  return cde < 0 ? 0 : (cde > f.qp.qmax ? f.qp.qmax : cde);
+}
+
+// Stages C (per-token stats / gate / V quantization) and D (K per-channel
+// quantization) for inputs that are exact in fp32 (fp16, bf16, fp32).  Only the
+// group extrema are formed in fp64 (from fp32 candidates within the error
+// bound), so the results equal the reference's fp64 arithmetic bit for bit.
+template <typename T>
+__device__ void encode_sides_fast(const DevCache& c, const EncSmem& sm, int side, int u, int b, int64_t start, int L,
+                                  int P, const float* p32, const double* p64, float pmax) {
+  const int tid = threadIdx.x;
+  const int D = c.D, Dp = c.Dp;
+  unsigned* nex = c.stats ? &c.stats[1] : nullptr;
+  auto m32at = [&](int idx, int cc) -> float {
+    return P <= 32 ? sm.ms[idx * sm.DS + cc] : p32[(int64_t)idx * Dp + cc];
+  };
+  const float INF = __int_as_float(0x7f800000);
+  const double DINF = __longlong_as_double(0x7ff0000000000000LL);
+
+  // ---- C. per-token stats (V always, K when the K gate is on) ----
+  // thread = (token t, channel half h): 64 channels each, partner in tid ^ 128,
+  // float4 row reads (conflict-free: row stride DS = 4 mod 32 words)
+  const bool per_token = (side == 1) || (c.use_kgate && P > 0);
+  if (per_token) {
+    const bool gate_on = side == 1 ? c.use_vgate : true;
+    double* diag = side == 1 ? c.vdiag : c.kdiag;
+    const int t = tid & (GMAX - 1), h = tid >> 7;
+    const int HC = (D + 1) / 2;                 // channels of half 0
+    const int c0 = h ? HC : 0, c1 = h ? D : HC;
+    float* xch = reinterpret_cast<float*>(sm.qlo);   // [2][GMAX][4] exchange (aliases qlo/qhi)
+    double* dch = sm.qlo;                            // [2][GMAX][2] after the first exchange
+    const bool act = t < L;
+    const int idx = act ? sm.fidx[t] : RAW;
+    const float* xr = sm.xs + t * sm.DS;
+    float xmx = -INF, xmn = INF, rmx = -INF, rmn = INF;
+    if (act) {
+      for (int cc = c0; cc < c1; ++cc) {
+        const float x = xr[cc];
+        xmx = fmaxf(xmx, x); xmn = fminf(xmn, x);
+        if (idx >= 0) {
+          const float r = x - m32at(idx, cc);
+          rmx = fmaxf(rmx, r); rmn = fminf(rmn, r);
+        }
+      }
+    }
+    __syncthreads();  // qlo/qhi free (the K path below reuses them only after its own barrier)
+    xch[(h * GMAX + t) * 4 + 0] = xmx; xch[(h * GMAX + t) * 4 + 1] = xmn;
+    xch[(h * GMAX + t) * 4 + 2] = rmx; xch[(h * GMAX + t) * 4 + 3] = rmn;
+    __syncthreads();
+    {
+      const float* o = xch + ((h ^ 1) * GMAX + t) * 4;
+      xmx = fmaxf(xmx, o[0]); xmn = fminf(xmn, o[1]); rmx = fmaxf(rmx, o[2]); rmn = fminf(rmn, o[3]);
+    }
+    const float S = act ? sm.xabs[t] + pmax : 0.f;
+    const float tol2 = 2.f * TWO_M22 * S;
+    const double* m = idx >= 0 ? p64 + (int64_t)idx * D : nullptr;
+    double clo = DINF, chi = -DINF;
+    if (act && idx >= 0) {
+      for (int cc = c0; cc < c1; ++cc) {
+        const float x = xr[cc];
+        const float r = x - m32at(idx, cc);
+        if (r <= rmn + tol2 || r >= rmx - tol2) {
+          const double r64 = __dsub_rn((double)x, m[cc]);
+          if (r <= rmn + tol2) clo = fmin(clo, r64);
+          if (r >= rmx - tol2) chi = fmax(chi, r64);
+        }
+      }
+    }
+    __syncthreads();
+    dch[(h * GMAX + t) * 2 + 0] = clo;
+    dch[(h * GMAX + t) * 2 + 1] = chi;
+    __syncthreads();
+    clo = fmin(clo, dch[((h ^ 1) * GMAX + t) * 2 + 0]);
+    chi = fmax(chi, dch[((h ^ 1) * GMAX + t) * 2 + 1]);
+    if (act) {
+      bool flatten = false;
+      if (idx >= 0) {
+        const double raw = __dsub_rn((double)xmx, (double)xmn), flat = __dsub_rn(chi, clo);
+        if (gate_on) flatten = raw > 0.0 && __ddiv_rn(flat, raw) <= c.thr;
+        else flatten = true;
+        if (h == 0 && c.keep_diag && diag) {
+          const int64_t o = ((int64_t)u * c.Tcap + start + t) * 2;
+          diag[o] = raw; diag[o + 1] = flat;
+        }
+      }
+      const int fidx = flatten ? idx : RAW;
+      if (side == 1) {
+        const double lo = flatten ? clo : (double)xmn, hi = flatten ? chi : (double)xmx;
+        const FastQ fq = make_fastq(lo, hi, c.qmax, flatten ? S : sm.xabs[t]);
+        uint8_t* crow = sm.codes + t * sm.CS;
+        for (int cc = c0; cc < c1; ++cc) {
+          const float x = xr[cc];
+          const float v32 = flatten ? x - m32at(idx, cc) : x;
+          crow[cc] = (uint8_t)fast_code(
+              v32, fq, [&]() { return flatten ? __dsub_rn((double)x, m[cc]) : (double)x; }, nex);
+        }
+        if (h == 0) {
+          const int64_t tok = (int64_t)u * c.Tcap + start + t;
+          const int64_t slot = ((int64_t)u * c.NBcap + b) * c.GP + t;
+          c.vparam64[2 * tok] = fq.qp.scale;
+          c.vparam64[2 * tok + 1] = fq.qp.lo;
+          c.vparam32[2 * slot] = (float)fq.qp.scale;
+          c.vparam32[2 * slot + 1] = (float)fq.qp.lo;
+          c.vidx[slot] = (int16_t)fidx;
+        }
+      }
+      if (side == 0 && h == 0) sm.fidx[t] = fidx;  // K gate choice (read by stage D after its barrier)
+    }
+  }
+
+  // ---- D. K: per-channel groups over the span's tokens ----
+  if (side == 0) {
+    __syncthreads();
+    const int ch = tid & (DMAX - 1), half = tid >> 7;
+    const int tb = half ? L / 2 : 0, te = half ? L : L / 2;
+    float* f32buf = reinterpret_cast<float*>(sm.qlo);  // [3][2][DMAX] floats (aliases qlo/qhi)
+    float mn = INF, mx = -INF, xab = 0.f;
+    bool anyp = false;
+    if (ch < D) {
+      for (int t = tb; t < te; ++t) {
+        const int idx = sm.fidx[t];
+        const float x = sm.xs[t * sm.DS + ch];
+        const float r = idx >= 0 ? x - m32at(idx, ch) : x;
+        mn = fminf(mn, r); mx = fmaxf(mx, r); xab = fmaxf(xab, fabsf(x));
+        anyp |= idx >= 0;
+      }
+    }
+    f32buf[(0 * 2 + half) * DMAX + ch] = mn;
+    f32buf[(1 * 2 + half) * DMAX + ch] = mx;
+    f32buf[(2 * 2 + half) * DMAX + ch] = anyp ? xab + pmax : xab;
+    __syncthreads();
+    mn = fminf(f32buf[ch], f32buf[DMAX + ch]);
+    mx = fmaxf(f32buf[2 * DMAX + ch], f32buf[3 * DMAX + ch]);
+    const float S = fmaxf(f32buf[4 * DMAX + ch], f32buf[5 * DMAX + ch]);
+    __syncthreads();
+    const float tol2 = 2.f * TWO_M22 * S;
+    double clo = DINF, chi = -DINF;
+    if (ch < D) {
+      for (int t = tb; t < te; ++t) {
+        const int idx = sm.fidx[t];
+        const float x = sm.xs[t * sm.DS + ch];
+        const float r = idx >= 0 ? x - m32at(idx, ch) : x;
+        if (r <= mn + tol2 || r >= mx - tol2) {
+          const double r64 = idx >= 0 ? __dsub_rn((double)x, p64[(int64_t)idx * D + ch]) : (double)x;
+          if (r <= mn + tol2) clo = fmin(clo, r64);
+          if (r >= mx - tol2) chi = fmax(chi, r64);
+        }
+      }
+    }
+    sm.qlo[half * DMAX + ch] = clo;
+    sm.qhi[half * DMAX + ch] = chi;
+    __syncthreads();
+    const double lo = fmin(sm.qlo[ch], sm.qlo[DMAX + ch]);
+    const double hi = fmax(sm.qhi[ch], sm.qhi[DMAX + ch]);
+    if (ch < D) {
+      const FastQ fq = make_fastq(lo, hi, c.qmax, S);
+      for (int t = tb; t < te; ++t) {
+        const int idx = sm.fidx[t];
+        const float x = sm.xs[t * sm.DS + ch];
+        const float r = idx >= 0 ? x - m32at(idx, ch) : x;
+        sm.codes[t * sm.CS + ch] = (uint8_t)fast_code(
+            r, fq, [&]() { return idx >= 0 ? __dsub_rn((double)x, p64[(int64_t)idx * D + ch]) : (double)x; }, nex);
+      }
+      if (half == 0) {
+        const int64_t o64 = ((int64_t)u * c.NBcap + b) * 2 * D;
+        c.kparam64[o64 + ch] = fq.qp.scale;
+        c.kparam64[o64 + D + ch] = fq.qp.lo;
+      }
+    }
+    if (half == 0) {
+      const int64_t o32 = ((int64_t)u * c.NBcap + b) * 2 * Dp;
+      for (int cc = ch; cc < Dp; cc += DMAX) {
+        float sc = 0.f, z = 0.f;
+        if (cc < D) { sc = (float)__ddiv_rn(__dsub_rn(hi, lo), (double)c.qmax); z = (float)lo; }
+        c.kparam32[o32 + cc] = sc;
+        c.kparam32[o32 + Dp + cc] = z;
+      }
+    }
+    for (int t = tid; t < L; t += ENC_THREADS) c.kidx[((int64_t)u * c.NBcap + b) * c.GP + t] = (int16_t)sm.fidx[t];
+  }
+}
+
+// Full fp32 d_mm of token t against pattern p, warp-cooperative (lane = 4 channels).
+__device__ __forceinline__ float coop_dmm(const EncSmem& sm, int t, int p, const float* p32, int Dp) {
+  const int lane = threadIdx.x & 31;
+  const int cc = 4 * lane;
+  float mx = -INF32, mn = INF32;
+  if (cc < sm.Dm) {
+    const float4 x4 = *reinterpret_cast<const float4*>(sm.xs + t * sm.DS + cc);
+    const float4 m4 = p < 32 ? *reinterpret_cast<const float4*>(sm.ms + p * sm.DS + cc)
+                             : __ldg(reinterpret_cast<const float4*>(p32 + (int64_t)p * Dp + cc));
+    const float r0 = x4.x - m4.x, r1 = x4.y - m4.y, r2 = x4.z - m4.z, r3 = x4.w - m4.w;
+    mx = fmax3(fmaxf(r0, r1), r2, r3);
+    mn = fmin3(fminf(r0, r1), r2, r3);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  return mx - mn;
+}
+
+// Exact nearest-pattern search with lower-bound pruning (P <= 64, inputs exact
+// in fp32).  LB_p = range over NPROBE channels of (x - m_p) <= d32(x, m_p)
+// exactly (same fp32 residuals, a subset of the channels), so every pattern
+// with LB_p > d*(p_guess) + 2 tol is farther than the winner by more than the
+// fp32 error window and never needs its full distance.  The survivors are
+// evaluated in full; the top-2 ambiguity test and fp64 re-match are the same
+// as the brute-force path, so indices stay bit-identical to the reference.
+template <typename T, bool TWO>
+__device__ void match_pruned(const DevCache& c, const EncSmem& sm, const SpanSrc<T>& src, int u, int64_t off, int L,
+                             int P, const float* p32, const double* p64, float pmax) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int D = c.D, Dp = c.Dp;
+  // ---- patterns 0..31 into ms, probe selection by pattern spread ----
+  for (int i = tid; i < 32 * sm.Dm; i += ENC_THREADS) {
+    const int p = i / sm.Dm, cc = i - p * sm.Dm;
+    sm.ms[p * sm.DS + cc] = p < P ? p32[(int64_t)p * Dp + (cc < D ? cc : 0)] : 0.f;
+  }
+  float* spread = sm.best1;  // [GMAX] scratch (unused by this path)
+  for (int ch = tid; ch < D; ch += ENC_THREADS) {
+    float lo = INF32, hi = -INF32;
+    for (int p = 0; p < P; ++p) {
+      const float m = p32[(int64_t)p * Dp + ch];
+      lo = fminf(lo, m); hi = fmaxf(hi, m);
+    }
+    spread[ch] = hi - lo;
+  }
+  __syncthreads();
+  const int np = D < NPROBE ? D : NPROBE;
+  for (int ch = tid; ch < D; ch += ENC_THREADS) {
+    const float sp = spread[ch];
+    int rank = 0;
+    for (int o = 0; o < D; ++o) rank += (spread[o] > sp) || (spread[o] == sp && o < ch);
+    if (rank < np) sm.probe[rank] = ch;
+  }
+  __syncthreads();
+  for (int i = tid; i < NPROBE * PRUNE_PMAX; i += ENC_THREADS) {
+    const int k = i / PRUNE_PMAX, p = i - k * PRUNE_PMAX;
+    const int ch = sm.probe[k < np ? k : 0];
+    sm.mpk[i] = p < P ? p32[(int64_t)p * Dp + ch] : 0.f;
+  }
+  __syncthreads();
+  int pr[NPROBE];
+  float m0[NPROBE], m1[TWO ? NPROBE : 1];
+#pragma unroll
+  for (int k = 0; k < NPROBE; ++k) {
+    pr[k] = sm.probe[k < np ? k : 0];
+    m0[k] = sm.mpk[k * PRUNE_PMAX + lane];
+    if constexpr (TWO) m1[k] = sm.mpk[k * PRUNE_PMAX + 32 + lane];
+  }
+  constexpr bool two = TWO;
+  const bool v0 = lane < P, v1 = lane + 32 < P;
+  for (int t0 = 16 * warp; t0 < 16 * warp + 16 && t0 < L; t0 += 4) {
+    float a0[4], b0[4], a1[4], b1[4];  // max/min of the probe residuals (pattern lane, lane+32)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { a0[j] = -INF32; b0[j] = INF32; a1[j] = -INF32; b1[j] = INF32; }
+#pragma unroll
+    for (int k = 0; k < NPROBE; k += 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float* xr = sm.xs + (t0 + j) * sm.DS;
+        const float xa = xr[pr[k]], xb = xr[pr[k + 1]];
+        const float ra = xa - m0[k], rb = xb - m0[k + 1];
+        a0[j] = fmax3(a0[j], ra, rb);
+        b0[j] = fmin3(b0[j], ra, rb);
+        if constexpr (TWO) {
+          const float sa = xa - m1[k], sb = xb - m1[k + 1];
+          a1[j] = fmax3(a1[j], sa, sb);
+          b1[j] = fmin3(b1[j], sa, sb);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      const int t = t0 + j;
+      if (t >= L) break;
+      const float lb0 = v0 ? a0[j] - b0[j] : INF32;
+      const float lb1 = v1 ? a1[j] - b1[j] : INF32;
+      // guess = lowest LB (lowest index on ties)
+      float gv = lb0 <= lb1 ? lb0 : lb1;
+      int gi = lb0 <= lb1 ? lane : lane + 32;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        if (ov < gv || (ov == gv && oi < gi)) { gv = ov; gi = oi; }
+      }
+      const float tol2 = 2.f * 9.5367431640625e-07f * (sm.xabs[t] + pmax);  // 2 * 2^-20 * S
+      float best = coop_dmm(sm, t, gi, p32, Dp);
+      int bi = gi;
+      float second = INF32;
+      const float bound = best + tol2;
+      unsigned c0 = __ballot_sync(0xffffffffu, lb0 <= bound);
+      unsigned c1 = __ballot_sync(0xffffffffu, lb1 <= bound);
+      if (gi < 32) c0 &= ~(1u << gi); else c1 &= ~(1u << (gi - 32));
+      const int ncand = __popc(c0) + __popc(c1);
+      if (ncand > PRUNE_MAXCAND) {
+        // poorly separated token: brute force over the whole table (lane = pattern)
+        float mx0 = -INF32, mn0 = INF32, mx1 = -INF32, mn1 = INF32;
+        const float* xr = sm.xs + t * sm.DS;
+        for (int cc = 0; cc < sm.Dm; cc += 4) {
+          const float4 x4 = *reinterpret_cast<const float4*>(xr + cc);
+          const float4 q0 = *reinterpret_cast<const float4*>(sm.ms + lane * sm.DS + cc);
+          const float r0 = x4.x - q0.x, r1 = x4.y - q0.y, r2 = x4.z - q0.z, r3 = x4.w - q0.w;
+          mx0 = fmax3(mx0, r0, r1); mx0 = fmax3(mx0, r2, r3);
+          mn0 = fmin3(mn0, r0, r1); mn0 = fmin3(mn0, r2, r3);
+          if (TWO && v1) {
+            const float4 q1 = __ldg(reinterpret_cast<const float4*>(p32 + (int64_t)(lane + 32) * Dp + cc));
+            const float s0 = x4.x - q1.x, s1 = x4.y - q1.y, s2 = x4.z - q1.z, s3 = x4.w - q1.w;
+            mx1 = fmax3(mx1, s0, s1); mx1 = fmax3(mx1, s2, s3);
+            mn1 = fmin3(mn1, s0, s1); mn1 = fmin3(mn1, s2, s3);
+          }
+        }
+        float va = v0 ? mx0 - mn0 : INF32, vb = v1 ? mx1 - mn1 : INF32;
+        float w1 = va <= vb ? va : vb, w2 = va <= vb ? vb : va;
+        int wi = va <= vb ? lane : lane + 32;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ob1 = __shfl_xor_sync(0xffffffffu, w1, o);
+          const int obi = __shfl_xor_sync(0xffffffffu, wi, o);
+          const float ob2 = __shfl_xor_sync(0xffffffffu, w2, o);
+          top2_merge(w1, wi, w2, ob1, obi, ob2);
+        }
+        best = w1; bi = wi; second = w2;
+      } else {
+        while (c0 | c1) {
+          int p;
+          if (c0) { p = __ffs(c0) - 1; c0 &= c0 - 1; }
+          else { p = 32 + __ffs(c1) - 1; c1 &= c1 - 1; }
+          const float d = coop_dmm(sm, t, p, p32, Dp);
+          if (d < best || (d == best && p < bi)) { second = best; best = d; bi = p; }
+          else second = fminf(second, d);
+        }
+      }
+      int idx = bi;
+      if (second <= best + tol2) {
+        idx = refine_match64<T>(sm, span_row(src, u, off, t, D), t, p64, P, D, lane);
+        if (lane == 0 && c.stats) atomicAdd(&c.stats[0], 1u);
+      }
+      if (lane == 0) sm.fidx[t] = idx;
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(ENC_THREADS, 2)
-encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block) {
+encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block, bool vec_rows) {
   const int u = blockIdx.y;
   const int b = first_block + blockIdx.x;
   const int64_t start = c.blk_start[b];
@@ -101,16 +493,19 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
   sm.xs = reinterpret_cast<float*>(smem_raw);
   sm.ms = sm.xs + GMAX * sm.DS;
   sm.codes = reinterpret_cast<uint8_t*>(sm.ms + 32 * sm.DS);
-  sm.xabs = reinterpret_cast<float*>(sm.codes + GMAX * Dp);
+  sm.CS = Dp + 4;
+  sm.xabs = reinterpret_cast<float*>(sm.codes + GMAX * sm.CS);
   sm.best1 = sm.xabs + GMAX;
   sm.best2 = sm.best1 + GMAX;
   sm.bidx = reinterpret_cast<int*>(sm.best2 + GMAX);
   sm.fidx = sm.bidx + GMAX;
   {
-    size_t o = (size_t)(GMAX + 32) * sm.DS * 4 + (size_t)GMAX * Dp + 6 * GMAX * 4;
+    size_t o = (size_t)(GMAX + 32) * sm.DS * 4 + (size_t)GMAX * sm.CS + 6 * GMAX * 4;
     o = (o + 15) / 16 * 16;
     sm.qlo = reinterpret_cast<double*>(smem_raw + o);
     sm.qhi = sm.qlo + 2 * DMAX;
+    sm.probe = reinterpret_cast<int*>(sm.qhi + 2 * DMAX);
+    sm.mpk = reinterpret_cast<float*>(sm.probe + NPROBE);
   }
   const int ntok = c.ntile_blk * 16;  // padded tokens in the block
 
@@ -123,26 +518,50 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
     const float pmax = P > 0 ? (side == 0 ? c.kpmax[u] : c.vpmax[u]) : 0.f;
 
     __syncthreads();  // previous side done with smem
-    // ---- A. stage rows as fp32, padded channels duplicate channel 0 ----------
-    for (int i = tid; i < L * sm.Dm; i += ENC_THREADS) {
-      int r = i / sm.Dm, cc = i - r * sm.Dm;
-      const T* row = span_row(src, u, off, r, D);
-      sm.xs[r * sm.DS + cc] = (float)to_f64(row[cc < D ? cc : 0]);
-    }
-    for (int i = tid; i < ntok * Dp; i += ENC_THREADS) {
-      int r = i / Dp, cc = i - r * Dp;
-      if (r >= L || cc >= D) sm.codes[i] = 0;
+    // ---- A. stage rows as fp32 (one row per warp, 16-byte loads), |x|max per row ----
+    {
+      constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte vector
+      for (int r = warp; r < L; r += ENC_THREADS / 32) {
+        const T* row = span_row(src, u, off, r, D);
+        float* xr = sm.xs + r * sm.DS;
+        float m = 0.f;
+        if (vec_rows) {
+          for (int ch = lane; ch < D / EPV; ch += 32) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + ch);
+            const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int q = 0; q < EPV; ++q) {
+              const float f = (float)to_f64(e[q]);
+              xr[ch * EPV + q] = f;
+              m = fmaxf(m, fabsf(f));
+            }
+          }
+        } else {
+          for (int ch = lane; ch < D; ch += 32) {
+            const float f = (float)to_f64(row[ch]);
+            xr[ch] = f;
+            m = fmaxf(m, fabsf(f));
+          }
+        }
+        m = warp_max_f(m);
+        __syncwarp();
+        if (lane < sm.Dm - D) xr[D + lane] = xr[0];  // padded channels duplicate channel 0
+        if (lane == 0) sm.xabs[r] = m;
+      }
+      // code tile padding: tokens >= L and channels >= D are zero codes
+      for (int r = L + warp; r < ntok; r += ENC_THREADS / 32)
+        for (int ch = lane; ch < Dp; ch += 32) sm.codes[r * sm.CS + ch] = 0;
+      if (D < Dp)
+        for (int r = warp; r < L; r += ENC_THREADS / 32)
+          for (int ch = D + lane; ch < Dp; ch += 32) sm.codes[r * sm.CS + ch] = 0;
     }
     __syncthreads();
-    for (int r = warp; r < L; r += ENC_THREADS / 32) {
-      float m = 0.f;
-      for (int cc = lane; cc < D; cc += 32) m = fmaxf(m, fabsf(sm.xs[r * sm.DS + cc]));
-      m = warp_max_f(m);
-      if (lane == 0) sm.xabs[r] = m;
-    }
 
-    // ---- B. fp32 min-max matching, lane = pattern ----------------------------
-    if (P > 0) {
+    // ---- B. fp32 min-max matching ------------------------------------------------
+    if (P > 0 && exact_in_f32<T>::value && P <= PRUNE_PMAX && c.prune) {
+      if (P > 32) match_pruned<T, true>(c, sm, src, u, off, L, P, p32, p64, pmax);
+      else match_pruned<T, false>(c, sm, src, u, off, L, P, p32, p64, pmax);
+    } else if (P > 0) {
       for (int pb = 0; pb < P; pb += 32) {
         const int pc = min(32, P - pb);
         __syncthreads();
@@ -208,126 +627,131 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
     }
     __syncthreads();
 
-    // ---- C. per-token residual stats, gate, and (V) per-token quantization ----
-    const bool per_token = (side == 1) || (c.use_kgate && P > 0);
-    if (per_token) {
-      const bool gate_on = side == 1 ? c.use_vgate : true;
-      double* diag = side == 1 ? c.vdiag : c.kdiag;
-      for (int t = warp; t < L; t += ENC_THREADS / 32) {
-        const T* row = span_row(src, u, off, t, D);
-        const int idx = sm.fidx[t];
-        const double* m = idx >= 0 ? p64 + (int64_t)idx * D : nullptr;
-        double xmx = -1.0 / 0.0, xmn = 1.0 / 0.0, rmx = xmx, rmn = xmn;
-        for (int cc = lane; cc < D; cc += 32) {
-          double x = xval<T>(sm, row, t, cc);
-          xmx = fmax(xmx, x); xmn = fmin(xmn, x);
-          if (m) { double r = __dsub_rn(x, m[cc]); rmx = fmax(rmx, r); rmn = fmin(rmn, r); }
-        }
-        xmx = warp_max_d(xmx); xmn = warp_min_d(xmn);
-        rmx = warp_max_d(rmx); rmn = warp_min_d(rmn);
-        bool flatten = false;
-        if (P > 0) {
-          const double raw = __dsub_rn(xmx, xmn), flat = __dsub_rn(rmx, rmn);
-          if (gate_on) flatten = raw > 0.0 && __ddiv_rn(flat, raw) <= c.thr;
-          else flatten = true;
-          if (lane == 0 && c.keep_diag && diag) {
-            int64_t o = ((int64_t)u * c.Tcap + start + t) * 2;
-            diag[o] = raw; diag[o + 1] = flat;
+    if constexpr (exact_in_f32<T>::value) {
+      encode_sides_fast<T>(c, sm, side, u, b, start, L, P, p32, p64, pmax);
+    } else {
+      // ---- fp64-input path: residuals, ranges and codes in IEEE fp64 ---------
+      const bool per_token = (side == 1) || (c.use_kgate && P > 0);
+      if (per_token) {
+        const bool gate_on = side == 1 ? c.use_vgate : true;
+        double* diag = side == 1 ? c.vdiag : c.kdiag;
+        for (int t = warp; t < L; t += ENC_THREADS / 32) {
+          const T* row = span_row(src, u, off, t, D);
+          const int idx = sm.fidx[t];
+          const double* m = idx >= 0 ? p64 + (int64_t)idx * D : nullptr;
+          double xmx = -1.0 / 0.0, xmn = 1.0 / 0.0, rmx = xmx, rmn = xmn;
+          for (int cc = lane; cc < D; cc += 32) {
+            double x = xval<T>(sm, row, t, cc);
+            xmx = fmax(xmx, x); xmn = fmin(xmn, x);
+            if (m) { double r = __dsub_rn(x, m[cc]); rmx = fmax(rmx, r); rmn = fmin(rmn, r); }
+          }
+          xmx = warp_max_d(xmx); xmn = warp_min_d(xmn);
+          rmx = warp_max_d(rmx); rmn = warp_min_d(rmn);
+          bool flatten = false;
+          if (P > 0) {
+            const double raw = __dsub_rn(xmx, xmn), flat = __dsub_rn(rmx, rmn);
+            if (gate_on) flatten = raw > 0.0 && __ddiv_rn(flat, raw) <= c.thr;
+            else flatten = true;
+            if (lane == 0 && c.keep_diag && diag) {
+              int64_t o = ((int64_t)u * c.Tcap + start + t) * 2;
+              diag[o] = raw; diag[o + 1] = flat;
+            }
+          }
+          const int fidx = flatten ? idx : RAW;
+          if (side == 0) {  // K gate: only the index/payload choice; K quantizes per channel below
+            __syncwarp();
+            if (lane == 0) sm.fidx[t] = fidx;
+            continue;
+          }
+          const double lo = flatten ? rmn : xmn, hi = flatten ? rmx : xmx;
+          const QuantParamsDev qp = make_qparams(lo, hi, c.qmax);
+          for (int cc = lane; cc < D; cc += 32) {
+            double x = xval<T>(sm, row, t, cc);
+            double v = flatten ? __dsub_rn(x, m[cc]) : x;
+            sm.codes[t * sm.CS + cc] = (uint8_t)quant_code(v, qp, c.stats ? &c.stats[1] : nullptr);
+          }
+          if (lane == 0) {
+            const int64_t tok = (int64_t)u * c.Tcap + start + t;
+            c.vparam64[2 * tok] = qp.scale;
+            c.vparam64[2 * tok + 1] = qp.lo;
+            const int64_t slot = ((int64_t)u * c.NBcap + b) * c.GP + t;
+            c.vparam32[2 * slot] = (float)qp.scale;
+            c.vparam32[2 * slot + 1] = (float)qp.lo;
+            c.vidx[slot] = (int16_t)fidx;
           }
         }
-        const int fidx = flatten ? idx : RAW;
-        if (side == 0) {  // K gate: only the index/payload choice; K quantizes per channel below
-          __syncwarp();
-          if (lane == 0) sm.fidx[t] = fidx;
-          continue;
-        }
-        const double lo = flatten ? rmn : xmn, hi = flatten ? rmx : xmx;
-        const QuantParamsDev qp = make_qparams(lo, hi, c.qmax);
-        for (int cc = lane; cc < D; cc += 32) {
-          double x = xval<T>(sm, row, t, cc);
-          double v = flatten ? __dsub_rn(x, m[cc]) : x;
-          sm.codes[t * Dp + cc] = (uint8_t)quant_code(v, qp, c.stats ? &c.stats[1] : nullptr);
-        }
-        if (lane == 0) {
-          const int64_t tok = (int64_t)u * c.Tcap + start + t;
-          c.vparam64[2 * tok] = qp.scale;
-          c.vparam64[2 * tok + 1] = qp.lo;
-          c.vparam32[2 * tok] = (float)qp.scale;
-          c.vparam32[2 * tok + 1] = (float)qp.lo;
-          c.vidx[tok] = (int16_t)fidx;
-        }
       }
-    }
 
-    // ---- D. K: per-channel quantization over the span's tokens ---------------
-    if (side == 0) {
-      __syncthreads();
-      const int ch = tid & (DMAX - 1), half = tid >> 7;
-      const int tb = half ? L / 2 : 0, te = half ? L : L / 2;
-      double lo = 1.0 / 0.0, hi = -1.0 / 0.0;
-      if (ch < D) {
-        for (int t = tb; t < te; ++t) {
-          const int idx = sm.fidx[t];
-          double x = xval<T>(sm, span_row(src, u, off, t, D), t, ch);
-          double v = idx >= 0 ? __dsub_rn(x, p64[(int64_t)idx * D + ch]) : x;
-          lo = fmin(lo, v); hi = fmax(hi, v);
+      // ---- D. K: per-channel quantization over the span's tokens ---------------
+      if (side == 0) {
+        __syncthreads();
+        const int ch = tid & (DMAX - 1), half = tid >> 7;
+        const int tb = half ? L / 2 : 0, te = half ? L : L / 2;
+        double lo = 1.0 / 0.0, hi = -1.0 / 0.0;
+        if (ch < D) {
+          for (int t = tb; t < te; ++t) {
+            const int idx = sm.fidx[t];
+            double x = xval<T>(sm, span_row(src, u, off, t, D), t, ch);
+            double v = idx >= 0 ? __dsub_rn(x, p64[(int64_t)idx * D + ch]) : x;
+            lo = fmin(lo, v); hi = fmax(hi, v);
+          }
         }
-      }
-      sm.qlo[half * DMAX + ch] = lo;
-      sm.qhi[half * DMAX + ch] = hi;
-      __syncthreads();
-      if (ch < D) {
-        lo = fmin(sm.qlo[ch], sm.qlo[DMAX + ch]);
-        hi = fmax(sm.qhi[ch], sm.qhi[DMAX + ch]);
-        const QuantParamsDev qp = make_qparams(lo, hi, c.qmax);
-        for (int t = tb; t < te; ++t) {
-          const int idx = sm.fidx[t];
-          double x = xval<T>(sm, span_row(src, u, off, t, D), t, ch);
-          double v = idx >= 0 ? __dsub_rn(x, p64[(int64_t)idx * D + ch]) : x;
-          sm.codes[t * Dp + ch] = (uint8_t)quant_code(v, qp, c.stats ? &c.stats[1] : nullptr);
+        sm.qlo[half * DMAX + ch] = lo;
+        sm.qhi[half * DMAX + ch] = hi;
+        __syncthreads();
+        if (ch < D) {
+          lo = fmin(sm.qlo[ch], sm.qlo[DMAX + ch]);
+          hi = fmax(sm.qhi[ch], sm.qhi[DMAX + ch]);
+          const QuantParamsDev qp = make_qparams(lo, hi, c.qmax);
+          for (int t = tb; t < te; ++t) {
+            const int idx = sm.fidx[t];
+            double x = xval<T>(sm, span_row(src, u, off, t, D), t, ch);
+            double v = idx >= 0 ? __dsub_rn(x, p64[(int64_t)idx * D + ch]) : x;
+            sm.codes[t * sm.CS + ch] = (uint8_t)quant_code(v, qp, c.stats ? &c.stats[1] : nullptr);
+          }
+          if (half == 0) {
+            const int64_t o64 = ((int64_t)u * c.NBcap + b) * 2 * D;
+            c.kparam64[o64 + ch] = qp.scale;
+            c.kparam64[o64 + D + ch] = qp.lo;
+          }
         }
         if (half == 0) {
-          const int64_t o64 = ((int64_t)u * c.NBcap + b) * 2 * D;
-          c.kparam64[o64 + ch] = qp.scale;
-          c.kparam64[o64 + D + ch] = qp.lo;
+          const int64_t o32 = ((int64_t)u * c.NBcap + b) * 2 * Dp;
+          for (int cc = ch; cc < Dp; cc += DMAX) {
+            float s = 0.f, z = 0.f;
+            if (cc < D) { s = (float)__ddiv_rn(__dsub_rn(hi, lo), (double)c.qmax); z = (float)lo; }
+            c.kparam32[o32 + cc] = s;
+            c.kparam32[o32 + Dp + cc] = z;
+          }
         }
+        for (int t = tid; t < L; t += ENC_THREADS) c.kidx[((int64_t)u * c.NBcap + b) * c.GP + t] = (int16_t)sm.fidx[t];
       }
-      if (half == 0) {
-        const int64_t o32 = ((int64_t)u * c.NBcap + b) * 2 * Dp;
-        for (int cc = ch; cc < Dp; cc += DMAX) {
-          float s = 0.f, z = 0.f;
-          if (cc < D) { s = (float)__ddiv_rn(__dsub_rn(hi, lo), (double)c.qmax); z = (float)lo; }
-          c.kparam32[o32 + cc] = s;
-          c.kparam32[o32 + Dp + cc] = z;
-        }
-      }
-      for (int t = tid; t < L; t += ENC_THREADS) c.kidx[(int64_t)u * c.Tcap + start + t] = (int16_t)sm.fidx[t];
     }
-
     // ---- E. pack the code tile into the mma-fragment layout -------------------
+    // thread = (lane ln, word group); words of one lane are contiguous in HBM
     __syncthreads();
     {
       const int WL = frag_words_per_lane(Dp, c.bits);
       const int S = 16 / c.bits;
-      const int words = c.ntile_blk * 32 * WL;
+      const int ln = tid & 31, grp = tid >> 5;
+      const int g = ln >> 2, q = ln & 3;
       uint32_t* dst = reinterpret_cast<uint32_t*>((side == 0 ? c.kcodes : c.vcodes) +
                                                   ((int64_t)u * c.NBcap + b) * c.blk_bytes);
-      for (int w = tid; w < words; w += ENC_THREADS) {
-        const int tile = w / (32 * WL);
-        const int rem = w - tile * 32 * WL;
-        const int ln = rem / WL, wl = rem - ln * WL;
+      for (int it = grp; it < c.ntile_blk * WL; it += ENC_THREADS / 32) {
+        const int tile = it / WL, wl = it - tile * WL;
         uint32_t word = 0;
-        for (int s = 0; s < S; ++s) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            FragPos p = frag_rc(ln, wl * S + s, e);
-            int tok, ch;
-            if (side == 0) { tok = tile * 16 + p.row; ch = 16 * p.j + p.col; }
-            else { ch = 16 * p.j + p.row; tok = tile * 16 + p.col; }
-            word |= (uint32_t)sm.codes[tok * Dp + ch] << ((e ? 16 : 0) + s * c.bits);
-          }
+        for (int s2 = 0; s2 < S; ++s2) {
+          const int R = wl * S + s2;
+          const int j = R >> 2, reg = R & 3;
+          const int row = g + 8 * (reg & 1), col = 2 * q + 8 * (reg >> 1);
+          const int shift = s2 * c.bits;
+          int t0, c0, t1, c1;  // element e = 0 and e = 1 (col and col + 1)
+          if (side == 0) { t0 = t1 = tile * 16 + row; c0 = 16 * j + col; c1 = c0 + 1; }
+          else { c0 = c1 = 16 * j + row; t0 = tile * 16 + col; t1 = t0 + 1; }
+          word |= (uint32_t)sm.codes[t0 * sm.CS + c0] << shift;
+          word |= (uint32_t)sm.codes[t1 * sm.CS + c1] << (16 + shift);
         }
-        dst[w] = word;
+        dst[(tile * 32 + ln) * WL + wl] = word;
       }
     }
   }
@@ -344,7 +768,10 @@ cudaError_t launch_encode(const DevCache& c, const SpanSrc<T>& k, const SpanSrc<
     attr_set = true;
   }
   dim3 grid(nblocks, c.U);
-  encode_span_kernel<T><<<grid, ENC_THREADS, smem, st>>>(c, k, v, first_block);
+  // 16-byte row loads need D * sizeof(T) % 16 == 0 and 16-byte aligned bases / unit strides
+  const bool vec = (c.D * sizeof(T)) % 16 == 0 && ((uintptr_t)k.base % 16) == 0 && ((uintptr_t)v.base % 16) == 0 &&
+                   (k.unit_stride * sizeof(T)) % 16 == 0 && (v.unit_stride * sizeof(T)) % 16 == 0;
+  encode_span_kernel<T><<<grid, ENC_THREADS, smem, st>>>(c, k, v, first_block, vec);
   return cudaGetLastError();
 }
 

@@ -144,12 +144,13 @@ __global__ void dequant_kernel(DevCache c, int nb, int64_t t0, int64_t n, double
     // K: scale_c * code + zero_c (+ pattern)   engine.py:255-261
     const double* kp = c.kparam64 + ((int64_t)u * c.NBcap + b) * 2 * c.D;
     double kv = __dadd_rn(__dmul_rn(kp[ch], (double)read_code(kb, 0, tb, ch, c.Dp, c.bits)), kp[c.D + ch]);
-    const int ki = c.kidx[(int64_t)u * c.Tcap + t];
+    const int64_t slot = ((int64_t)u * c.NBcap + b) * c.GP + tb;
+    const int ki = c.kidx[slot];
     if (ki >= 0) kv = __dadd_rn(kv, c.kpat64[((int64_t)u * c.Pcap + ki) * c.D + ch]);
     // V: scale_t * code + zero_t (+ pattern)   engine.py:264-268
     const double* vp = c.vparam64 + ((int64_t)u * c.Tcap + t) * 2;
     double vv = __dadd_rn(__dmul_rn(vp[0], (double)read_code(vb, 1, tb, ch, c.Dp, c.bits)), vp[1]);
-    const int vi = c.vidx[(int64_t)u * c.Tcap + t];
+    const int vi = c.vidx[slot];
     if (vi >= 0) vv = __dadd_rn(vv, c.vpat64[((int64_t)u * c.Pcap + vi) * c.D + ch]);
     kout[((int64_t)u * n + (i / c.D)) * c.D + ch] = kv;
     vout[((int64_t)u * n + (i / c.D)) * c.D + ch] = vv;

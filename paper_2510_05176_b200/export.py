@@ -82,8 +82,10 @@ def export_unit(cache: PatternKVCache, u: int, with_bytes: bool = True) -> UnitS
     nb = len(kb_start)
     kp = _arena(cache, "kparam64", torch.float64, ()).view(cache.n_units, -1, 2, D)[u, :nb].cpu().numpy()
     vp = _arena(cache, "vparam64", torch.float64, ()).view(cache.n_units, -1, 2)[u, :Cn].cpu().numpy()
-    kidx = _arena(cache, "kidx", torch.int16, ())[u, :Cn].to(torch.int32).cpu().numpy()
-    vidx = _arena(cache, "vidx", torch.int16, ())[u, :Cn].to(torch.int64).cpu().numpy()
+    gp = 16 * ((cfg.group_size + 15) // 16)
+    slots = np.concatenate([b * gp + np.arange(int(n)) for b, n in enumerate(kb_len)]) if nb else np.zeros(0, np.int64)
+    kidx = _arena(cache, "kidx", torch.int16, ())[u].cpu().numpy()[slots].astype(np.int32)
+    vidx = _arena(cache, "vidx", torch.int16, ())[u].cpu().numpy()[slots].astype(np.int64)
     kc, vc = cache.codes(0, Cn)
     kc_u, vc_u = kc[u], vc[u]
     vdec = np.zeros((0, 3))
