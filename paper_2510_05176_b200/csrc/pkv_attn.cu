@@ -44,18 +44,27 @@ __device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
   return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
 }
 
-// Dequantize slot s (0..16/bits-1) of a code word into a half2 of exact code values.
+// Dequantize slot s of a code word into the half2 (1024 + 2^k c_lo, 1024 + 2^k c_hi),
+// k = frag_slot_shift(s): one LOP3 (plus a shared byte shift for the upper slots).
+// The constant 1024 and the per-channel 2^k are removed exactly outside the MMA
+// (K: folded into B and a per-block bias; V: per-row correction of the output).
 template <int BITS>
-__device__ __forceinline__ uint32_t slot_h2(uint32_t w, int s) {
-  constexpr int PER = BITS == 2 ? 4 : (BITS == 4 ? 2 : 1);  // slots extractable without shifting
+__device__ __forceinline__ uint32_t slot_raw(uint32_t w, int s) {
+  constexpr int PER = 8 / BITS;  // slots in the low byte of each half
   const uint32_t ww = s >= PER ? (w >> 8) : w;
   const int ss = s >= PER ? s - PER : s;
   const uint32_t mask = ((1u << BITS) - 1) * 0x00010001u << (ss * BITS);
-  const uint32_t v = lop3_magic(ww, mask);
-  // (1024 + 2^(ss*BITS) c) * 2^-(ss*BITS) - 1024 * 2^-(ss*BITS) = c exactly
-  const float sc = 1.f / (float)(1 << (ss * BITS));
+  return lop3_magic(ww, mask);
+}
+
+// exact code values (c_lo, c_hi): raw value * 2^-k - 1024 * 2^-k in one HFMA2
+template <int BITS>
+__device__ __forceinline__ uint32_t slot_exact(uint32_t w, int s) {
+  constexpr int PER = 8 / BITS;
+  const int k = (s % PER) * BITS;
+  const float sc = 1.f / (float)(1 << k);
   const __half hs = __float2half_rn(sc), hb = __float2half_rn(-1024.f * sc);
-  return hfma2_u(v, pack_h2(hs, hs), pack_h2(hb, hb));
+  return hfma2_u(slot_raw<BITS>(w, s), pack_h2(hs, hs), pack_h2(hb, hb));
 }
 
 template <int BITS>
@@ -110,13 +119,15 @@ __device__ __forceinline__ void load_stage_words(const unsigned char* p, uint32_
 }
 
 // A fragments of sub-tile j (4 half2 registers) from the lane's code words.
-template <int BITS>
+template <int BITS, int SIDE>
 __device__ __forceinline__ void afrag(const uint32_t* w, int j, uint32_t* a) {
-  constexpr int S = 16 / BITS;
 #pragma unroll
   for (int reg = 0; reg < 4; ++reg) {
-    const int R = 4 * j + reg;
-    a[reg] = slot_h2<BITS>(w[R / S], R % S);
+    int word, slot;
+    frag_word_slot(SIDE, 4 * j + reg, BITS, word, slot);
+    // K: raw 1024 + 2^k c (bias and 2^k folded into B); V: exact c (the PV
+    // accumulator runs over thousands of tiles and must not carry the bias)
+    a[reg] = SIDE == 0 ? slot_raw<BITS>(w[word], slot) : slot_exact<BITS>(w[word], slot);
   }
 }
 
@@ -191,33 +202,49 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
   unsigned char* ring = reinterpret_cast<unsigned char*>(sred + ATT_WARPS * MAXG * 4) + (size_t)warp * ATT_STAGES * SB;
   constexpr int tbytes = 16 * Dp * BITS / 8;
   int pb = b0 + warp, pti = 0;                  // producer cursor
-  int pnt = pb < b1 ? (c.blk_len[pb] + 15) >> 4 : 0;
+  int pnt = 0;
+  // per-lane source pointers of the producer block: K/V code slices, and the
+  // 16-byte metadata slice this lane moves (lanes 0-1 kidx, 2-3 vidx, 4-11 vparam)
+  const uint8_t* ksrc = nullptr;
+  const uint8_t* vsrc = nullptr;
+  const uint8_t* msrc = nullptr;
+  const int minc = lane < 4 ? 32 : 128;         // metadata bytes per tile for this lane's array
+  auto set_block = [&]() {
+    if (pb >= b1) return;
+    const int64_t bo = (int64_t)u * c.NBcap + pb;
+    pnt = (c.blk_len[pb] + 15) >> 4;
+    ksrc = c.kcodes + bo * c.blk_bytes + lane * KCB;
+    vsrc = c.vcodes + bo * c.blk_bytes + lane * KCB;
+    const int64_t slot = bo * c.GP;
+    msrc = lane < 2 ? reinterpret_cast<const uint8_t*>(c.kidx + slot) + 16 * lane
+         : lane < 4 ? reinterpret_cast<const uint8_t*>(c.vidx + slot) + 16 * (lane - 2)
+                    : reinterpret_cast<const uint8_t*>(c.vparam32 + 2 * slot) + 16 * (lane - 4);
+  };
+  set_block();
   auto issue = [&](int stage) {
     unsigned char* st = ring + stage * SB;
     if (pb < b1) {
-      const int64_t bo = (int64_t)u * c.NBcap + pb;
-      const uint8_t* ksrc = c.kcodes + bo * c.blk_bytes + pti * tbytes + lane * KCB;
-      const uint8_t* vsrc = c.vcodes + bo * c.blk_bytes + pti * tbytes + lane * KCB;
-      if ((KCB & 15) == 0) {
+      if constexpr ((KCB & 15) == 0) {
+#pragma unroll
         for (int o = 0; o < KCB; o += 16) {
           cp_async16(st + lane * KCB + o, ksrc + o);
           cp_async16(st + 32 * KCB + lane * KCB + o, vsrc + o);
         }
       } else {
+#pragma unroll
         for (int o = 0; o < KCB; o += 4) {
           cp_async4(st + lane * KCB + o, ksrc + o);
           cp_async4(st + 32 * KCB + lane * KCB + o, vsrc + o);
         }
       }
-      const int64_t slot = bo * c.GP + pti * 16;
-      unsigned char* meta = st + 64 * KCB;
-      if (lane < 2) cp_async16(meta + 16 * lane, reinterpret_cast<const uint8_t*>(c.kidx + slot) + 16 * lane);
-      else if (lane < 4) cp_async16(meta + 32 + 16 * (lane - 2), reinterpret_cast<const uint8_t*>(c.vidx + slot) + 16 * (lane - 2));
-      else if (lane < 12) cp_async16(meta + 64 + 16 * (lane - 4), reinterpret_cast<const uint8_t*>(c.vparam32 + 2 * slot) + 16 * (lane - 4));
+      if (lane < 12) cp_async16(st + 64 * KCB + 16 * lane, msrc);
+      ksrc += tbytes;
+      vsrc += tbytes;
+      msrc += minc;
       if (++pti == pnt) {
         pti = 0;
         pb += ATT_WARPS;
-        pnt = pb < b1 ? (c.blk_len[pb] + 15) >> 4 : 0;
+        set_block();
       }
     }
     cp_async_commit();
@@ -226,38 +253,47 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
   for (int s = 0; s < ATT_STAGES - 1; ++s) issue(s);
 
   uint32_t bq[8][NT][2];
-  float qz[NT];
+  float qz[NT], kbias[NT];
   int L = 0;
   int stage = 0;
   for (int b = b0 + warp; b < b1; b += ATT_WARPS) {
     L = c.blk_len[b];
     const float* kp = c.kparam32 + ((int64_t)u * c.NBcap + b) * 2 * Dp;
-    // B fragments of q o s_b (hi/lo columns) and q.z_b per head
+    // B fragments of 64 * 2^-k(c) * (q o s_b) (hi/lo columns), q.z_b per head, and
+    // the per-column bias 1024 * sum_c B[c][col] the magic-number A operand adds
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int col = 8 * nt + g, h = col >> 1, hl = col & 1;
-      float zpart = 0.f;
+      float zpart = 0.f, bpart = 0.f;
 #pragma unroll
       for (int kt = 0; kt < 8; ++kt) {
         if (kt < KT) {
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int ch = 16 * kt + 2 * qd + 8 * hh;
+            constexpr int HS = 8 / BITS;
+            const float fk = (float)(64 >> frag_slot_shift(2 * (kt % HS) + hh, BITS));  // 2^(6-k)
             const float2 s2 = __ldg(reinterpret_cast<const float2*>(kp + ch));
             const float2 z2 = __ldg(reinterpret_cast<const float2*>(kp + Dp + ch));
             const float q0 = sq[h * Dp + ch], q1 = sq[h * Dp + ch + 1];
-            const float t0 = q0 * s2.x, t1 = q1 * s2.y;
-            const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
-            __half e0 = h0, e1 = h1;
-            if (hl) { e0 = __float2half_rn(t0 - __half2float(h0)); e1 = __float2half_rn(t1 - __half2float(h1)); }
-            bq[kt][nt][hh] = pack_h2(e0, e1);
+            const float t0 = q0 * s2.x * fk, t1 = q1 * s2.y * fk;
+            const __half2 hi = __floats2half2_rn(t0, t1);
+            const float2 bk = __half22float2(hi);
+            const __half2 lo = __floats2half2_rn(t0 - bk.x, t1 - bk.y);
+            const __half2 e = hl ? lo : hi;
+            const float2 ef = __half22float2(e);
+            bpart += ef.x + ef.y;
+            bq[kt][nt][hh] = *reinterpret_cast<const uint32_t*>(&e);
             zpart = fmaf(q0, z2.x, fmaf(q1, z2.y, zpart));
           }
         }
       }
       zpart += __shfl_xor_sync(0xffffffffu, zpart, 1);
       zpart += __shfl_xor_sync(0xffffffffu, zpart, 2);
+      bpart += __shfl_xor_sync(0xffffffffu, bpart, 1);
+      bpart += __shfl_xor_sync(0xffffffffu, bpart, 2);
       qz[nt] = __shfl_sync(0xffffffffu, zpart, 8 * qd);  // head 4nt+qd lives at g = 2qd
+      kbias[nt] = 1024.f * (__shfl_sync(0xffffffffu, bpart, 8 * qd) + __shfl_sync(0xffffffffu, bpart, 8 * qd + 4));
     }
     const int ntile = (L + 15) >> 4;
     for (int ti = 0; ti < ntile; ++ti) {
@@ -272,7 +308,7 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       const float2* mp = reinterpret_cast<const float2*>(st + 64 * KCB + 64);
       const int r0 = 16 * ti + g, r1 = r0 + 8;
       const bool ok0 = r0 < L, ok1 = r1 < L;
-      const int ki0 = ok0 ? mk[g] : -1, ki1 = ok1 ? mk[g + 8] : -1;
+      const int ki0 = mk[g], ki1 = mk[g + 8];
       const int vi0 = ok0 ? mv[g] : -1, vi1 = ok1 ? mv[g + 8] : -1;
       const float2 vp0 = ok0 ? mp[g] : make_float2(0.f, 0.f);
       const float2 vp1 = ok1 ? mp[g + 8] : make_float2(0.f, 0.f);
@@ -290,7 +326,7 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       for (int kt = 0; kt < 8; ++kt) {
         if (kt < KT) {
           uint32_t af[4];
-          afrag<BITS>(kw, kt, af);
+          afrag<BITS, 0>(kw, kt, af);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) mma16816(sacc[nt], af, bq[kt][nt][0], bq[kt][nt][1]);
         }
@@ -299,10 +335,10 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int h = 4 * nt + qd;
-        const float add0 = qz[nt] + (ki0 >= 0 ? sqm[ki0 * MAXG + min(h, MAXG - 1)] : 0.f);
-        const float add1 = qz[nt] + (ki1 >= 0 ? sqm[ki1 * MAXG + min(h, MAXG - 1)] : 0.f);
-        const float s0 = ok0 ? (sacc[nt][0] + sacc[nt][1] + add0) * a.scale_log2 : -INFINITY;
-        const float s1 = ok1 ? (sacc[nt][2] + sacc[nt][3] + add1) * a.scale_log2 : -INFINITY;
+        const float add0 = qz[nt] + (ki0 >= 0 && ok0 ? sqm[ki0 * MAXG + h] : 0.f);
+        const float add1 = qz[nt] + (ki1 >= 0 && ok1 ? sqm[ki1 * MAXG + h] : 0.f);
+        const float s0 = ok0 ? fmaf(sacc[nt][0] + sacc[nt][1] - kbias[nt], 0.015625f, add0) * a.scale_log2 : -INFINITY;
+        const float s1 = ok1 ? fmaf(sacc[nt][2] + sacc[nt][3] - kbias[nt], 0.015625f, add1) * a.scale_log2 : -INFINITY;
         float tmax = fmaxf(s0, s1);
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
@@ -335,10 +371,11 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
           if (vi1 >= 0 && p1 != 0.f) atomicAdd(wslot(vi1, nt), p1);
         }
         const float w0 = p0 * vp0.x, w1 = p1 * vp1.x;
-        const __half w0h = __float2half_rn(w0), w1h = __float2half_rn(w1);
-        const __half w0l = __float2half_rn(w0 - __half2float(w0h)), w1l = __float2half_rn(w1 - __half2float(w1h));
-        *reinterpret_cast<uint32_t*>(myP + g * 16 + 8 * nt + 2 * qd) = pack_h2(w0h, w0l);
-        *reinterpret_cast<uint32_t*>(myP + (g + 8) * 16 + 8 * nt + 2 * qd) = pack_h2(w1h, w1l);
+        const __half2 wh = __floats2half2_rn(w0, w1);
+        const float2 wb = __half22float2(wh);
+        const __half2 wl = __floats2half2_rn(w0 - wb.x, w1 - wb.y);
+        *reinterpret_cast<__half2*>(myP + g * 16 + 8 * nt + 2 * qd) = __halves2half2(__low2half(wh), __low2half(wl));
+        *reinterpret_cast<__half2*>(myP + (g + 8) * 16 + 8 * nt + 2 * qd) = __halves2half2(__high2half(wh), __high2half(wl));
       }
       __syncwarp();
       // ---- O^T += V^T . P~ : channels on M ----
@@ -354,7 +391,7 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       for (int mt = 0; mt < 8; ++mt) {
         if (mt < KT) {
           uint32_t af[4];
-          afrag<BITS>(vw, mt, af);
+          afrag<BITS, 1>(vw, mt, af);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) mma16816(oacc[mt][nt], af, bp[nt][0], bp[nt][1]);
         }
@@ -515,9 +552,7 @@ static cudaError_t launch_chunks_kt(const DevCache& c, const AttnArgs& a, size_t
 template <int BITS, int NT>
 static cudaError_t launch_chunks(const DevCache& c, const AttnArgs& a, size_t smem, cudaStream_t st) {
   switch (c.Dp / 16) {
-    case 2: return launch_chunks_kt<BITS, NT, 2>(c, a, smem, st);
     case 4: return launch_chunks_kt<BITS, NT, 4>(c, a, smem, st);
-    case 6: return launch_chunks_kt<BITS, NT, 6>(c, a, smem, st);
     default: return launch_chunks_kt<BITS, NT, 8>(c, a, smem, st);
   }
 }

@@ -257,7 +257,7 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
   c->cfg = *cfg;
   c->U = n_units;
   c->D = head_dim;
-  c->Dp = round_up(head_dim, 32);
+  c->Dp = round_up(head_dim, 64);  // whole k-tile groups of the fragment layout at every bit width
   c->dtype = in_dtype;
   c->esize = esize_of(in_dtype);
   c->flags = flags;
@@ -278,6 +278,7 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
   auto bail = [&](int code) { pkv_cache_destroy(c); return code; };
   if (dalloc(&d.kpmax, (size_t)n_units * 4) || dalloc(&d.vpmax, (size_t)n_units * 4) ||
       dalloc(&d.nk, (size_t)n_units * 4) || dalloc(&d.nv, (size_t)n_units * 4) ||
+      dalloc(&d.probe, (size_t)n_units * 2 * 16 * 4) ||
       dalloc(&d.wk, (size_t)n_units * d.Wcap * head_dim * c->esize) ||
       dalloc(&d.wv, (size_t)n_units * d.Wcap * head_dim * c->esize) || dalloc(&c->scratch_flag, 8))
     return bail(fail(PKV_CUDA, -1, "cudaMalloc failed: %s", cudaGetErrorString(cudaGetLastError())));
@@ -294,7 +295,7 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
 extern "C" int pkv_cache_destroy(pkv_cache* c) {
   if (!c) return PKV_OK;
   DevCache& d = c->dev;
-  void* ptrs[] = {d.kpat64, d.vpat64, d.kpat32, d.vpat32, d.kpmax, d.vpmax, d.nk, d.nv, d.blk_start, d.blk_len,
+  void* ptrs[] = {d.kpat64, d.vpat64, d.kpat32, d.vpat32, d.kpmax, d.vpmax, d.nk, d.nv, d.probe, d.blk_start, d.blk_len,
                   d.kcodes, d.kparam32, d.kparam64, d.kidx, d.vcodes, d.vparam32, d.vparam64, d.vidx, d.kdiag,
                   d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag};
   for (void* p : ptrs)
@@ -337,6 +338,7 @@ extern "C" int pkv_cache_reset(pkv_cache* c, int32_t keep_patterns, void* stream
     CU(cudaMemsetAsync(c->dev.kpmax, 0, (size_t)c->U * 4, st));
     CU(cudaMemsetAsync(c->dev.vpmax, 0, (size_t)c->U * 4, st));
     c->pk_bound = c->pv_bound = 0;
+    CU(launch_probes(c->dev, st));
   }
   return PKV_OK;
 }
@@ -477,6 +479,7 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
     CU(cudaFreeAsync(p, st));
   if (side_mask & 1) c->pk_bound = k;
   if (side_mask & 2) c->pv_bound = k;
+  CU(launch_probes(c->dev, st));
   return PKV_OK;
 }
 
@@ -515,6 +518,7 @@ extern "C" int pkv_set_patterns(pkv_cache* c, int32_t side, const double* pat, i
   CU(cudaMemcpyAsync(p32, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(side == 0 ? d.kpmax : d.vpmax, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(side == 0 ? d.nk : d.nv, n.data(), n.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(launch_probes(d, st));
   CU(cudaStreamSynchronize(st));
   if (side == 0) c->pk_bound = P; else c->pv_bound = P;
   return PKV_OK;
@@ -607,6 +611,7 @@ extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stre
         CU(e);
         if (mask & 1) c->pk_bound += 1;
         if (mask & 2) c->pv_bound += 1;
+        CU(launch_probes(d, st));
       }
     }
     // commit the oldest G rows against the refreshed tables (engine.py:195)

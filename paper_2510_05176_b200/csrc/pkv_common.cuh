@@ -128,14 +128,17 @@ __device__ __forceinline__ int quant_code(double v, const QuantParamsDev& p, uns
 }
 
 // ---- fragment layout ---------------------------------------------------------------
-// Within a 16-token tile, 32 lanes x (Dp*bits/64) 32-bit words.  Word `wl` of
-// lane `lane` holds 16/bits half2 "slots"; slot s covers register R = wl*S+s
-// of the lane's mma.m16n8k16 A fragments (4 per 16x16 sub-tile): sub-tile
-// j = R/4, reg = R%4, row = g + 8*(reg&1), col = 2q + 8*(reg>>1) + e with
-// g = lane/4, q = lane%4, e = half index (low/high 16 bits).  Code bits sit at
-// (e ? 16 : 0) + s*bits inside the word.
-//   K tile (A = K, M = tokens, K-dim = channels): token = row, channel = 16j+col
-//   V tile (A = V^T, M = channels, K-dim = tokens): channel = 16j+row, token = col
+// Within a 16-token tile, 32 lanes x (Dp*bits/64) 32-bit words.  Lane l holds the
+// 4*KT mma.m16n8k16 A-fragment registers R = 4j + reg of its sub-tiles j (K: k-tiles
+// over channels; V: m-tiles over channels), reg = hiRow + 2*hiCol, each register a
+// half2 of elements (row, col) = (g + 8*hiRow, 2q + 8*hiCol + e), g = l/4, q = l%4.
+//   K tile (A = K, M = tokens, K-dim = channels):  token = row, channel = 16j + col
+//   V tile (A = V^T, M = channels, K-dim = tokens): channel = 16j + row, token = col
+// Register R lives in word `word` at half2 slot `slot` (code bits at
+// (e ? 16 : 0) + slot*bits).  The slot depends only on the operand's CHANNEL
+// index (K: (j, hiCol); V: (j, hiRow)), so the power-of-two factor left by the
+// LOP3 magic-number dequant (1024 + 2^k code) is constant per channel and folds
+// into B (K) or the output rows (V) instead of costing an HFMA2 per element.
 struct FragPos { int j, row, col; };  // sub-tile, row in [0,16), col in [0,16)
 __device__ __forceinline__ FragPos frag_rc(int lane, int R, int e) {
   int reg = R & 3;
@@ -145,6 +148,22 @@ __device__ __forceinline__ FragPos frag_rc(int lane, int R, int e) {
   p.col = 2 * (lane & 3) + 8 * (reg >> 1) + e;
   return p;
 }
+__host__ __device__ __forceinline__ void frag_word_slot(int side, int R, int bits, int& word, int& slot) {
+  const int j = R >> 2, reg = R & 3, hiRow = reg & 1, hiCol = reg >> 1, HS = 8 / bits;
+  const int inner = side == 0 ? hiCol : hiRow, outer = side == 0 ? hiRow : hiCol;
+  word = outer + 2 * (j / HS);
+  slot = 2 * (j % HS) + inner;
+}
+// inverse: (word, slot) -> register R
+__host__ __device__ __forceinline__ int frag_reg_of(int side, int word, int slot, int bits) {
+  const int HS = 8 / bits;
+  const int j = (word >> 1) * HS + (slot >> 1);
+  const int inner = slot & 1, outer = word & 1;
+  const int hiRow = side == 0 ? outer : inner, hiCol = side == 0 ? inner : outer;
+  return 4 * j + hiRow + 2 * hiCol;
+}
+// bit shift k of the dequantized value 1024 + 2^k * code for a slot
+__host__ __device__ constexpr int frag_slot_shift(int slot, int bits) { return (slot % (8 / bits)) * bits; }
 // words per lane per tile, bytes per tile
 __host__ __device__ inline int frag_words_per_lane(int Dp, int bits) { return Dp * bits / 64; }
 __host__ __device__ inline int tile_bytes(int Dp, int bits) { return 16 * Dp * bits / 8; }
@@ -162,6 +181,7 @@ struct DevCache {
   double* kpat64; double* vpat64;
   float* kpat32; float* vpat32;
   float* kpmax; float* vpmax;     // max |m| over each unit's table (filter tolerance)
+  int* probe;                     // [U][2][16] probe channels of the pruned matcher
   int* nk; int* nv;               // per-unit pattern counts
   // blocks
   int64_t* blk_start; int* blk_len;  // [NBcap] (lockstep across units)
@@ -227,5 +247,6 @@ cudaError_t launch_unpack(const uint8_t*, int64_t, int, uint8_t*, cudaStream_t);
 cudaError_t launch_match(const double*, int64_t, const double*, int, int, int64_t*, double*, double*, cudaStream_t);
 cudaError_t launch_midrange(const double*, int64_t, int, double*, cudaStream_t);
 size_t mine_smem_bytes(int k, int D);
+cudaError_t launch_probes(const DevCache&, cudaStream_t);
 
 }  // namespace pkv

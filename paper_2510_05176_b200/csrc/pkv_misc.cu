@@ -102,21 +102,57 @@ template cudaError_t launch_refresh<__nv_bfloat16>(const DevCache&, int, int, in
 template cudaError_t launch_refresh<float>(const DevCache&, int, int, int, cudaStream_t);
 template cudaError_t launch_refresh<double>(const DevCache&, int, int, int, cudaStream_t);
 
+// ---- probe channels of the pruned matcher: the 16 channels with the largest
+// spread (max - min over the fp32 table) of each unit-side, ties to the lowest
+// channel.  Recomputed whenever a table changes (mining, install, refresh).
+__global__ void probe_kernel(DevCache c) {
+  const int u = blockIdx.x, side = blockIdx.y, ch = threadIdx.x;
+  const int P = side == 0 ? (c.use_kp ? c.nk[u] : 0) : (c.use_vp ? c.nv[u] : 0);
+  const float* p32 = (side == 0 ? c.kpat32 : c.vpat32) + (int64_t)u * c.Pcap * c.Dp;
+  __shared__ float spread[DMAX];
+  if (ch < c.D) {
+    float lo = 3.0e38f, hi = -3.0e38f;
+    for (int p = 0; p < P; ++p) {
+      const float v = p32[(int64_t)p * c.Dp + ch];
+      lo = fminf(lo, v); hi = fmaxf(hi, v);
+    }
+    spread[ch] = P > 0 ? hi - lo : 0.f;
+  }
+  __syncthreads();
+  int* out = c.probe + ((int64_t)u * 2 + side) * 16;
+  const int np = c.D < 16 ? c.D : 16;
+  if (ch < c.D) {
+    const float sp = spread[ch];
+    int rank = 0;
+    for (int o = 0; o < c.D; ++o) rank += (spread[o] > sp) || (spread[o] == sp && o < ch);
+    if (rank < np) out[rank] = ch;
+  }
+  __syncthreads();
+  if (ch >= np && ch < 16) out[ch] = out[0];
+}
+cudaError_t launch_probes(const DevCache& c, cudaStream_t st) {
+  probe_kernel<<<dim3(c.U, 2), DMAX, 0, st>>>(c);
+  return cudaGetLastError();
+}
+
 // ---- fragment-layout addressing (inverse of frag_rc) -------------------------------
 struct CodeLoc { int word; int shift; };
-__device__ __forceinline__ CodeLoc frag_locate(int row, int col16, int j, int bits, int WL) {
+__device__ __forceinline__ CodeLoc frag_locate(int side, int row, int col16, int j, int bits, int WL) {
   // row/col16 are the A-fragment coordinates inside sub-tile j
   const int g = row & 7, hr = row >> 3, q = (col16 & 7) >> 1, hc = col16 >> 3, e = col16 & 1;
-  const int reg = hr + 2 * hc, lane = 4 * g + q, R = 4 * j + reg, S = 16 / bits;
+  const int reg = hr + 2 * hc, lane = 4 * g + q, R = 4 * j + reg;
+  int word, slot;
+  frag_word_slot(side, R, bits, word, slot);
   CodeLoc l;
-  l.word = lane * WL + R / S;
-  l.shift = (e ? 16 : 0) + (R % S) * bits;
+  l.word = lane * WL + word;
+  l.shift = (e ? 16 : 0) + slot * bits;
   return l;
 }
 __device__ __forceinline__ int read_code(const uint8_t* blk, int side, int tok, int ch, int Dp, int bits) {
   const int WL = frag_words_per_lane(Dp, bits);
   const int tile = tok >> 4;
-  CodeLoc l = side == 0 ? frag_locate(tok & 15, ch & 15, ch >> 4, bits, WL) : frag_locate(ch & 15, tok & 15, ch >> 4, bits, WL);
+  CodeLoc l = side == 0 ? frag_locate(0, tok & 15, ch & 15, ch >> 4, bits, WL)
+                        : frag_locate(1, ch & 15, tok & 15, ch >> 4, bits, WL);
   const uint32_t w = reinterpret_cast<const uint32_t*>(blk + (size_t)tile * tile_bytes(Dp, bits))[l.word];
   return (w >> l.shift) & ((1 << bits) - 1);
 }

@@ -192,6 +192,7 @@ def test_decode_attention_vs_fp64_oracle(pkv, bits, gqa):
         vall = np.concatenate([vc[u].cpu().numpy(), wv[u].double().cpu().numpy()])
         ref = O.attention(q[u].astype(np.float64), kall, vall, 1.0 / math.sqrt(d))
         err = np.abs(out[u] - ref).max() / np.abs(ref).max()
+        print(f"bits={bits} gqa={gqa} unit={u} max-abs err / max|ref| = {err:.3e}")
         assert err <= 1e-3, (u, err)
 
 
