@@ -246,7 +246,7 @@ cudaError_t launch_pack(const uint8_t*, int64_t, int, uint8_t*, cudaStream_t);
 cudaError_t launch_unpack(const uint8_t*, int64_t, int, uint8_t*, cudaStream_t);
 cudaError_t launch_match(const double*, int64_t, const double*, int, int, int64_t*, double*, double*, cudaStream_t);
 cudaError_t launch_midrange(const double*, int64_t, int, double*, cudaStream_t);
-size_t mine_smem_bytes(int k, int D);
+size_t mine_smem_bytes(int k, int D, bool tc);
 cudaError_t launch_probes(const DevCache&, cudaStream_t);
 
 }  // namespace pkv

@@ -12,18 +12,37 @@
 //     (patterns.py:112-118), centers = means (patterns.py:119-120) summed
 //     sequentially in point order exactly like numpy's axis-0 reduction, and
 //     the rel-tol 1e-6 stop (patterns.py:121-125).
-// Squared distances are fp64 FMA chains (the reference's einsum order is CPU
-// specific; mining is "parity-unpinned at ulp level").
+// Squared distances: v1 path = fp64 FMA chains on CUDA cores; tensor-core path
+// (fp16 inputs, d = 128, k <= 64) = the T x k x d product on tcgen05: TMA streams
+// 128-point tiles of X (fp16, exact) into 128B-swizzled smem, one thread issues
+// tcgen05.mma kind::f16 against the centers split hi+lo into two fp16 columns,
+// accumulating in TMEM; four epilogue warps read the accumulator with tcgen05.ld
+// and take the argmin of ||c||^2 - 2 x.c, re-deciding in fp64 any point whose two
+// best candidates lie within the error bound.  The objective and the centroid
+// means stay fp64 on CUDA cores (O(T d) per round).  The reference's einsum order
+// is CPU specific, so mining is "parity-unpinned at ulp level".
 #include "pkv_common.cuh"
+#include "pkv_sm100.cuh"
+
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 namespace pkv {
 
-constexpr int MINE_THREADS = 512;
+constexpr int MINE_THREADS = 256;
 constexpr int KMAX = 96;
 constexpr int KCH = 16;  // centers per register chunk
 
 struct MineSmem {
-  double* cen;    // [k][D]
+  double* cen;    // [k][CST] (CST = D + 1: conflict-free per-thread row reads)
+  int CST;
+  // tensor-core assignment (TC path only)
+  unsigned char* sA;  // [2 stages][2 K-halves][128 rows x 128 B], 1024-aligned, 128B swizzle
+  unsigned char* sB;  // [2 K-halves][NP rows x 128 B]
+  float* cc;          // [NP/2] ||c_j||^2 (+inf for padding)
+  uint64_t* bars;     // full[2], empty[2], tfull[2], tempty[2]
+  uint32_t* tmem;     // TMEM base address
   int* cnt;       // [KMAX]
   int* off;       // [KMAX]
   int* wcnt;      // [16][KMAX]
@@ -102,7 +121,7 @@ __device__ double assign_pass(const T* X, int64_t Tn, int D, int k, MineSmem& sm
 #pragma unroll
         for (int j = 0; j < KCH; ++j) {
           if (j0 + j < k) {
-            double d = __dsub_rn(xv, sm.cen[(j0 + j) * D + c]);
+            double d = __dsub_rn(xv, sm.cen[(j0 + j) * sm.CST + c]);
             acc[j] = fma(d, d, acc[j]);
           }
         }
@@ -123,8 +142,182 @@ __device__ double assign_pass(const T* X, int64_t Tn, int D, int k, MineSmem& sm
   return obj;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, MineArgs<T> a) {
+// ---------------------------------------------------------------------------------
+// tensor-core assignment pass (fp16 points, d = 128, k <= 64)
+// ---------------------------------------------------------------------------------
+constexpr int TC_TILE = 128;
+constexpr int TC_EPI_WARP0 = 4;  // warps 4..7: epilogue, TMEM lane quarter = warp % 4
+
+__host__ __device__ inline int tc_np(int k) { return ((2 * k + 15) / 16) * 16; }
+
+__device__ __forceinline__ unsigned char* tc_sa(const MineSmem& sm, int stage, int half) {
+  return sm.sA + (stage * 2 + half) * (TC_TILE * 128);
+}
+
+// fp64 squared distance of smem point row r (swizzled fp16 tile) to center j
+__device__ __forceinline__ double tc_d2_exact(const MineSmem& sm, int stage, int row, int j) {
+  double acc = 0.0;
+  const double* cj = sm.cen + j * sm.CST;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const unsigned char* base = tc_sa(sm, stage, half) + row * 128;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + ((ch ^ (row & 7)) << 4));
+      const __half* hv = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double d = __dsub_rn((double)__half2float(hv[e]), cj[half * 64 + ch * 8 + e]);
+        acc = fma(d, d, acc);
+      }
+    }
+  }
+  return acc;
+}
+
+// One assignment pass over the T points of this unit-side.  Returns this thread's
+// share of sum_t d2(x_t, c[lab_old[t]]) (fp64) when lab_old != nullptr.
+__device__ double assign_tc(int64_t Tn, int k, MineSmem& sm, const int* lab_old, int* lab_new, bool count,
+                            const CUtensorMap* map, int64_t row_base, uint32_t& gtile) {
+  using namespace sm100;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NP = tc_np(k);
+  const int NT = (int)((Tn + TC_TILE - 1) / TC_TILE);
+  uint64_t* full = sm.bars;
+  uint64_t* empty = sm.bars + 2;
+  uint64_t* tfull = sm.bars + 4;
+  uint64_t* tempty = sm.bars + 6;
+  if (count)
+    for (int j = tid; j < k; j += MINE_THREADS) sm.cnt[j] = 0;
+  // B operand: row 2j = hi(c_j), row 2j+1 = lo(c_j) = fp16(c_j - hi), K-major, 128B swizzle
+  for (int i = tid; i < NP * 16; i += MINE_THREADS) {
+    const int row = i >> 4, half = (i >> 3) & 1, chunk = i & 7;
+    const int j = row >> 1, part = row & 1;
+    __half hv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      __half h = __float2half(0.f);
+      if (j < k) {
+        const double cv = sm.cen[j * sm.CST + half * 64 + chunk * 8 + e];
+        const __half hi = __double2half(cv);
+        h = part == 0 ? hi : __double2half(cv - (double)__half2float(hi));
+      }
+      hv[e] = h;
+    }
+    *reinterpret_cast<uint4*>(sm.sB + half * NP * 128 + row * 128 + ((chunk ^ (row & 7)) << 4)) =
+        *reinterpret_cast<const uint4*>(hv);
+  }
+  for (int j = tid; j < NP / 2; j += MINE_THREADS) {
+    double a = 0.0;
+    if (j < k)
+      for (int c = 0; c < 128; ++c) a = fma(sm.cen[j * sm.CST + c], sm.cen[j * sm.CST + c], a);
+    sm.cc[j] = j < k ? (float)a : __int_as_float(0x7f800000);
+  }
+  fence_proxy_async();
+  __syncthreads();
+  float ccmax = 0.f;
+  for (int j = 0; j < k; ++j) ccmax = fmaxf(ccmax, sm.cc[j]);
+  const float cnorm = sqrtf(ccmax);
+  double obj = 0.0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int m = 0; m < NT; ++m) {
+        const uint32_t g = gtile + m, s = g & 1, ph = (g >> 1) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], 2 * TC_TILE * 128);
+        const int r0 = (int)(row_base + (int64_t)m * TC_TILE);
+        tma_load_2d(tc_sa(sm, s, 0), map, &full[s], 0, r0);
+        tma_load_2d(tc_sa(sm, s, 1), map, &full[s], 64, r0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16_f32(TC_TILE, NP);
+      const uint64_t db0 = smem_desc_k_sw128(sm.sB), db1 = smem_desc_k_sw128(sm.sB + NP * 128);
+      for (int m = 0; m < NT; ++m) {
+        const uint32_t g = gtile + m, s = g & 1, ph = (g >> 1) & 1;
+        const uint32_t acc = g & 1, aph = (g >> 1) & 1;
+        mbar_wait(&full[s], ph);
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint64_t da0 = smem_desc_k_sw128(tc_sa(sm, s, 0)), da1 = smem_desc_k_sw128(tc_sa(sm, s, 1));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over d = 128 (two 64-wide swizzle halves)
+          const uint64_t da = (kk < 4 ? da0 : da1) + 2 * (kk & 3);  // +32 B per K step
+          const uint64_t db = (kk < 4 ? db0 : db1) + 2 * (kk & 3);
+          mma_f16_ss(*sm.tmem + acc * 128, da, db, idesc, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= TC_EPI_WARP0 && warp < TC_EPI_WARP0 + 4) {
+    const int q = warp & 3, row = 32 * q + lane;
+    for (int m = 0; m < NT; ++m) {
+      const uint32_t g = gtile + m, s = g & 1, acc = g & 1, aph = (g >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int64_t t = (int64_t)m * TC_TILE + row;
+      float vb = __int_as_float(0x7f800000), vs = vb;
+      int bi = 0;
+      for (int c0 = 0; c0 < NP; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(*sm.tmem + acc * 128 + c0 + ((uint32_t)(32 * q) << 16), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int j = c0 / 2 + e;
+          const float dot = __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]);
+          const float val = fmaf(-2.f, dot, sm.cc[j]);
+          if (val < vb) { vs = vb; vb = val; bi = j; }
+          else vs = fminf(vs, val);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (t < Tn) {
+        // |x|^2 for the error bound; fp64 objective against the previous labels
+        float xx = 0.f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const unsigned char* base = tc_sa(sm, s, half) + row * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const uint4 w = *reinterpret_cast<const uint4*>(base + ((ch ^ (row & 7)) << 4));
+            const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(h2[e]);
+              xx = fmaf(f.x, f.x, fmaf(f.y, f.y, xx));
+            }
+          }
+        }
+        if (lab_old) obj += tc_d2_exact(sm, s, row, lab_old[t]);
+        // |err(||c||^2 - 2 x.c)| <= 2^-16 |x||c| + 2^-21 (|c|^2 + |x|^2): B split (2^-22),
+        // tensor-core fp32 accumulation over 8 K-steps, fp32 roundings (K2)
+        const float tol = 1.52587890625e-05f * sqrtf(xx) * cnorm + 4.76837158203125e-07f * (ccmax + xx);
+        if (vs - vb <= 2.f * tol) {  // near tie: decide in fp64 (reference arithmetic, lowest index)
+          double best = __longlong_as_double(0x7ff0000000000000LL);
+          for (int j = 0; j < k; ++j) {
+            const double d = tc_d2_exact(sm, s, row, j);
+            if (d < best) { best = d; bi = j; }
+          }
+        }
+        lab_new[t] = bi;
+        if (count) atomicAdd(&sm.cnt[bi], 1);
+      }
+      mbar_arrive(&empty[s]);
+    }
+  }
+  gtile += NT;
+  __syncthreads();
+  return obj;
+}
+
+template <typename T, bool TC>
+__global__ void __launch_bounds__(MINE_THREADS, 1)
+kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
   const int u = blockIdx.x, side = blockIdx.y;
   if (!((a.side_mask >> side) & 1)) return;
   const int D = c.D, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -142,14 +335,45 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MineSmem sm;
-  sm.cen = reinterpret_cast<double*>(smem_raw);
-  sm.redv = sm.cen + (size_t)k * D;
+  sm.CST = D + 1;
+  unsigned char* sbase = smem_raw;
+  if (TC) {
+    // 1024-aligned swizzled operand tiles first
+    const uintptr_t p = reinterpret_cast<uintptr_t>(smem_raw);
+    sbase = reinterpret_cast<unsigned char*>((p + 1023) & ~(uintptr_t)1023);
+    sm.sA = sbase;
+    sm.sB = sm.sA + 4 * TC_TILE * 128;
+    sbase = sm.sB + 2 * tc_np(k) * 128;
+  }
+  sm.cen = reinterpret_cast<double*>(sbase);
+  sm.redv = sm.cen + (size_t)k * sm.CST;
   sm.redi = reinterpret_cast<long long*>(sm.redv + 32);
   sm.cnt = reinterpret_cast<int*>(sm.redi + 32);
   sm.off = sm.cnt + KMAX;
   sm.wcnt = sm.off + KMAX;
   sm.chosen = sm.wcnt + 16 * KMAX;
   sm.flags = sm.chosen + KMAX;
+  uint32_t gtile = 0;
+  const CUtensorMap* tmap = side == 0 ? &tmK : &tmV;
+  if (TC) {
+    sm.bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(sm.flags + 4 + 1) & ~(uintptr_t)7);
+    sm.tmem = reinterpret_cast<uint32_t*>(sm.bars + 8);
+    sm.cc = reinterpret_cast<float*>(sm.tmem + 4);
+    if (tid == 0) {
+      for (int i = 0; i < 2; ++i) {
+        sm100::mbar_init(&sm.bars[i], 1);                       // full: producer arrive + tx
+        sm100::mbar_init(&sm.bars[2 + i], 128);                 // empty: epilogue threads
+        sm100::mbar_init(&sm.bars[4 + i], 1);                   // tmem full: MMA commit
+        sm100::mbar_init(&sm.bars[6 + i], 128);                 // tmem empty: epilogue threads
+      }
+      sm100::fence_mbar_init();
+      sm100::tma_prefetch(tmap);
+    }
+    if (warp == 1) sm100::tmem_alloc<256>(sm.tmem);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+  }
 
   // ---- seeding (patterns.py:134-142) with distinct-rows detection --------------
   const int64_t first = a.first[side][u];
@@ -198,7 +422,7 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
           if (x1 > x2) break;
         }
       }
-      for (int cc = 0; cc < D; ++cc) sm.cen[rank * D + cc] = to_f64(ri[cc]);
+      for (int cc = 0; cc < D; ++cc) sm.cen[rank * sm.CST + cc] = to_f64(ri[cc]);
     }
     __syncthreads();
     assign_pass(X, Tn, D, n, sm, nullptr, lab, own, false);
@@ -207,10 +431,12 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
   } else {
     for (int i = tid; i < k * D; i += MINE_THREADS) {
       int j = i / D, cc = i - j * D;
-      sm.cen[i] = to_f64(X[(int64_t)sm.chosen[j] * D + cc]);
+      sm.cen[j * sm.CST + cc] = to_f64(X[(int64_t)sm.chosen[j] * D + cc]);
     }
     __syncthreads();
-    assign_pass(X, Tn, D, k, sm, nullptr, lab, own, true);
+    if (TC) assign_tc(Tn, k, sm, nullptr, lab, true, tmap, (int64_t)u * Tn, gtile);
+    else assign_pass(X, Tn, D, k, sm, nullptr, lab, own, true);
+    bool own_valid = !TC;  // the TC pass computes labels only; own d2 is rebuilt on demand
     double prev = 1.0 / 0.0;
     for (int it = 0; it < 25; ++it) {
       // ---- empty-cluster repair (patterns.py:112-118) ----------------------------
@@ -221,6 +447,16 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
       }
       __syncthreads();
       const int ne = sm.flags[0];
+      if (ne > 0 && !own_valid) {  // rare: exact fp64 d2 to the assigned centers
+        for (int64_t t = tid; t < Tn; t += MINE_THREADS) {
+          const T* xr = X + t * D;
+          const double* cj = sm.cen + lab[t] * sm.CST;
+          double acc = 0.0;
+          for (int cc = 0; cc < D; ++cc) { const double d = __dsub_rn(to_f64(xr[cc]), cj[cc]); acc = fma(d, d, acc); }
+          own[t] = acc;
+        }
+        __syncthreads();
+      }
       for (int ei = 0; ei < ne; ++ei) {
         const int e = sm.off[ei];
         double bv = -1.0 / 0.0; long long bi = 0x7fffffffffffffffLL;
@@ -278,11 +514,13 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
         const int* lj = list + sm.off[j];
         double s = to_f64(X[(int64_t)lj[0] * D + cc]);
         for (int q = 1; q < n_j; ++q) s = __dadd_rn(s, to_f64(X[(int64_t)lj[q] * D + cc]));
-        sm.cen[i] = __ddiv_rn(s, (double)n_j);
+        sm.cen[j * sm.CST + cc] = __ddiv_rn(s, (double)n_j);
       }
       __syncthreads();
       // ---- objective of this round fused with the next assignment ----------------
-      double part = assign_pass(X, Tn, D, k, sm, lab, lab2, near_, true);
+      double part = TC ? assign_tc(Tn, k, sm, lab, lab2, true, tmap, (int64_t)u * Tn, gtile)
+                       : assign_pass(X, Tn, D, k, sm, lab, lab2, near_, true);
+      own_valid = !TC;
       const double obj = block_sum(part, sm);
       if (tid == 0) hist[it] = obj;
       iters = it + 1;
@@ -298,7 +536,7 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
   float amax = 0.f;
   for (int i = tid; i < n * D; i += MINE_THREADS) {
     const int j = i / D, cc = i - j * D;
-    const double v = sm.cen[i];
+    const double v = sm.cen[j * sm.CST + cc];
     p64[(int64_t)j * D + cc] = v;
     p32[(int64_t)j * c.Dp + cc] = (float)v;
     amax = fmaxf(amax, fabsf((float)v) * (1.f + 1e-6f));
@@ -321,17 +559,64 @@ __global__ void __launch_bounds__(MINE_THREADS, 1) kmeans_kernel(DevCache c, Min
     const int* fin = lab;
     for (int64_t t = tid; t < Tn; t += MINE_THREADS) a.labels_out[so + t] = fin[t];
   }
+  if (TC) {
+    __syncthreads();
+    if (warp == 1) sm100::tmem_free<256>(*sm.tmem);
+  }
 }
 
-size_t mine_smem_bytes(int k, int D) {
-  return (size_t)k * D * 8 + 32 * 8 + 32 * 8 + (size_t)(KMAX * 3 + 16 * KMAX + 4) * 4;
+size_t mine_smem_bytes(int k, int D, bool tc) {
+  size_t b = (size_t)k * (D + 1) * 8 + 32 * 8 + 32 * 8 + (size_t)(KMAX * 3 + 16 * KMAX + 4 + 2) * 4;
+  if (tc) b += 1024 + 4 * TC_TILE * 128 + 2 * (size_t)tc_np(k) * 128 + 8 * 8 + 16 + (size_t)tc_np(k) / 2 * 4 + 64;
+  return b;
+}
+
+// TMA descriptor of a [rows][128] fp16 matrix, 64 x 128 boxes, 128-byte swizzle
+static bool make_tmap(CUtensorMap* map, const void* base, uint64_t rows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return false;
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  const cuuint64_t dims[2] = {128, rows};
+  const cuuint64_t strides[1] = {128 * 2};
+  const cuuint32_t box[2] = {64, TC_TILE};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <typename T>
 cudaError_t launch_mine(const DevCache& c, const MineArgs<T>& a, cudaStream_t st) {
-  size_t smem = mine_smem_bytes(a.k, c.D);
-  cudaFuncSetAttribute(kmeans_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kmeans_kernel<T><<<dim3(c.U, 2), MINE_THREADS, smem, st>>>(c, a);
+  CUtensorMap tk, tv;
+  memset(&tk, 0, sizeof tk);
+  memset(&tv, 0, sizeof tv);
+  bool tc = false;
+  if constexpr (std::is_same<T, __half>::value) {
+    const char* env = getenv("PKV_MINE_CUDA_CORES");
+    tc = c.D == 128 && a.k <= 64 && a.unit_stride == a.T * 128 && !(env && env[0] == '1') &&
+         make_tmap(&tk, a.x[0], (uint64_t)c.U * a.T) && make_tmap(&tv, a.x[1], (uint64_t)c.U * a.T);
+  }
+  const size_t smem = mine_smem_bytes(a.k, c.D, tc);
+  if constexpr (std::is_same<T, __half>::value) {
+    if (tc) {
+      cudaFuncSetAttribute(kmeans_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kmeans_kernel<T, true><<<dim3(c.U, 2), MINE_THREADS, smem, st>>>(c, a, tk, tv);
+      return cudaGetLastError();
+    }
+  }
+  {
+    cudaFuncSetAttribute(kmeans_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kmeans_kernel<T, false><<<dim3(c.U, 2), MINE_THREADS, smem, st>>>(c, a, tk, tv);
+  }
   return cudaGetLastError();
 }
 

@@ -211,3 +211,34 @@ def test_errors_map_to_reference_taxonomy(pkv):
     v[0, 3, 1] = float("inf")
     with pytest.raises(DataError, match="token 3"):
         cache.prefill(k, v, validate=True)
+
+
+@pytest.mark.parametrize("k", [16, 32, 64])
+def test_tcgen05_mining_matches_cuda_core_and_oracle(pkv, k, monkeypatch):
+    """K2 on tcgen05 (fp16, d=128) == the fp64 CUDA-core miner bit for bit, and
+    == the oracle's k-means within 1e-12 (einsum-order ulps only)."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, T, d = 3, 2048, 128
+    xs = []
+    for u in range(U):
+        kk, vv = O.synth_unit(O.unit_seed(2, 1, u), T, d)
+        xs.append(kk.astype(np.float16).astype(np.float64) if u % 2 == 0 else vv.astype(np.float16).astype(np.float64))
+    x = torch.from_numpy(np.stack(xs)).half().cuda()
+    ec = EngineConfig(bits=2, pattern_count=k)
+    tabs = {}
+    for mode in ("tc", "cuda_core"):
+        if mode == "cuda_core":
+            monkeypatch.setenv("PKV_MINE_CUDA_CORES", "1")
+        cache = pkv.PatternKVCache(ec, U, d, dtype=torch.float16, max_tokens=T + 256)
+        hist, nit = cache.mine(0, x, seed=7)
+        nk, _ = cache.pattern_counts()
+        tabs[mode] = (cache.patterns(0)[:, :k].cpu().numpy(), hist, nit, nk)
+    np.testing.assert_array_equal(tabs["tc"][0], tabs["cuda_core"][0])
+    np.testing.assert_array_equal(tabs["tc"][2], tabs["cuda_core"][2])
+    for u in range(U):
+        cen, lab, hist = O.kmeans(xs[u], k, 7)
+        assert tabs["tc"][3][u] == len(cen)
+        np.testing.assert_allclose(tabs["tc"][0][u, :len(cen)], cen, rtol=0, atol=1e-12)
+        assert int(tabs["tc"][2][u]) == len(hist)
+        np.testing.assert_allclose(tabs["tc"][1][u, :len(hist)], hist, rtol=1e-12)

@@ -1,0 +1,91 @@
+"""Write the committed evidence under profiles/ from ncu reports in gpurun_out/.
+
+    python tools/make_profiles.py <round-tag>
+
+For each full capture (prof_*_full.ncu-rep / prof_kmeans.ncu-rep) writes a text
+summary (SOL metrics, DRAM traffic, tensor-pipe activity, instruction mix, hot
+source lines) and a traffic.json consumed by bench.py for roofline.traffic; the
+launch list (launches.csv) is summarised per kernel (share of the step).
+"""
+
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+import ncu_summary  # noqa: E402
+
+
+def run(cmd):
+    return subprocess.run(cmd, capture_output=True, text=True).stdout
+
+
+def lines(rep, top=30):
+    return run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, str(top)])
+
+
+def launch_summary(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(list)
+    for r in data:
+        if len(r) > vi:
+            agg[r[ki].split("(")[0][:90]].append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for v in agg.values())
+    out = ["kernel | launches | mean ms | share of all kernel time"]
+    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+        out.append(f"{k} | {len(v)} | {sum(v) / len(v) / 1e6:.3f} | {sum(v) / tot * 100:.1f}%")
+    return "\n".join(out)
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "round1"
+    os.makedirs(PROF, exist_ok=True)
+    traffic = {}
+    for name in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn"):
+        rep = os.path.join(OUT, name + ".ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        txt = "\n".join(ncu_summary.details(rep))
+        raw = ncu_summary.raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
+                                    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                                    "gpu__time_duration.sum", "launch__grid_size"])
+        txt += "\n" + "\n".join(f"{k:60s} {v[0]} {v[1]}" for k, v in raw.items())
+        txt += "\n\n" + "\n".join(ncu_summary.sass(rep, nwin=0))
+        txt += "\n\nhot source lines (share of executed instructions / of stall samples):\n" + lines(rep)
+        with open(os.path.join(PROF, f"{tag}_{name}.txt"), "w") as f:
+            f.write(f"# ncu --set full capture: {name}.ncu-rep ({tag})\n\n" + txt)
+        if name.endswith("_full") and "dram__bytes_read.sum" in raw:
+            def to_bytes(v):
+                val, unit = float(v[0].replace(",", "")), v[1]
+                return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+            traffic[name.replace("prof_", "").replace("_full", "")] = (
+                to_bytes(raw["dram__bytes_read.sum"]) + to_bytes(raw["dram__bytes_write.sum"]))
+    if traffic:
+        with open(os.path.join(PROF, "traffic.json"), "w") as f:
+            json.dump({"source": f"ncu --set full, bench configuration ({tag})", "bytes_per_launch": traffic}, f,
+                      indent=1)
+    lp = os.path.join(OUT, "launches.csv")
+    if os.path.exists(lp):
+        with open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w") as f:
+            f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 "
+                    "python bench.py --steps 2 --warmup 3 --no-four-bit --no-cpu\n"
+                    "# cold-cache, serialised launches: compare shares, not absolutes\n\n")
+            f.write(launch_summary(lp) + "\n")
+        import shutil
+        shutil.copy(lp, os.path.join(PROF, f"{tag}_launches.csv"))
+    print("wrote", sorted(os.listdir(PROF)))
+
+
+if __name__ == "__main__":
+    main()
