@@ -40,6 +40,12 @@ __device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) 
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
   return r;
 }
+// register transpose of an 8x8 b16 tile held in mma C/A-fragment order
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+  uint32_t r;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
 __device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
   return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
 }
@@ -317,21 +323,27 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       stage = (stage + 1) % ATT_STAGES;
 
       // ---- S = K . (q o s): tokens on M, hi/lo head columns on N ----
-      float sacc[NT][4];
+      // two accumulator chains (even / odd k-tiles) halve the dependent-MMA latency
+      float sacc[NT][4], sacc2[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) sacc[nt][r] = 0.f;
+        for (int r = 0; r < 4; ++r) { sacc[nt][r] = 0.f; sacc2[nt][r] = 0.f; }
 #pragma unroll
       for (int kt = 0; kt < 8; ++kt) {
         if (kt < KT) {
           uint32_t af[4];
           afrag<BITS, 0>(kw, kt, af);
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma16816(sacc[nt], af, bq[kt][nt][0], bq[kt][nt][1]);
+          for (int nt = 0; nt < NT; ++nt) mma16816((kt & 1) ? sacc2[nt] : sacc[nt], af, bq[kt][nt][0], bq[kt][nt][1]);
         }
       }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) sacc[nt][r] += sacc2[nt][r];
       // ---- online softmax (lazy rescale), P~ = p * s_t split hi/lo ----
+      uint32_t pt[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int h = 4 * nt + qd;
@@ -374,19 +386,15 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
         const __half2 wh = __floats2half2_rn(w0, w1);
         const float2 wb = __half22float2(wh);
         const __half2 wl = __floats2half2_rn(w0 - wb.x, w1 - wb.y);
-        *reinterpret_cast<__half2*>(myP + g * 16 + 8 * nt + 2 * qd) = __halves2half2(__low2half(wh), __low2half(wl));
-        *reinterpret_cast<__half2*>(myP + (g + 8) * 16 + 8 * nt + 2 * qd) = __halves2half2(__high2half(wh), __high2half(wl));
+        // P~ rows g / g+8 (cols 2qd, 2qd+1 = hi, lo of head 4nt+qd) are C-fragment
+        // 8x8 b16 tiles; their transposes are exactly the PV B fragments (k = token, n = col)
+        const __half2 r0 = __halves2half2(__low2half(wh), __low2half(wl));
+        const __half2 r1 = __halves2half2(__high2half(wh), __high2half(wl));
+        pt[nt][0] = movmatrix_t(*reinterpret_cast<const uint32_t*>(&r0));
+        pt[nt][1] = movmatrix_t(*reinterpret_cast<const uint32_t*>(&r1));
       }
-      __syncwarp();
       // ---- O^T += V^T . P~ : channels on M ----
-      uint32_t bp[NT][2];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int col = 8 * nt + g;
-        bp[nt][0] = pack_h2(myP[(2 * qd) * 16 + col], myP[(2 * qd + 1) * 16 + col]);
-        bp[nt][1] = pack_h2(myP[(2 * qd + 8) * 16 + col], myP[(2 * qd + 9) * 16 + col]);
-      }
-      __syncwarp();
+      uint32_t (&bp)[NT][2] = pt;
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
         if (mt < KT) {

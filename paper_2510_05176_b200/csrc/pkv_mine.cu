@@ -268,10 +268,12 @@ __device__ double assign_tc(int64_t Tn, int k, MineSmem& sm, const int* lab_old,
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int j = c0 / 2 + e;
-          const float dot = __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]);
-          const float val = fmaf(-2.f, dot, sm.cc[j]);
-          if (val < vb) { vs = vb; vb = val; bi = j; }
-          else vs = fminf(vs, val);
+          if (j < k) {  // columns past N (last 32-column load) are not centers
+            const float dot = __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]);
+            const float val = fmaf(-2.f, dot, sm.cc[j]);
+            if (val < vb) { vs = vb; vb = val; bi = j; }
+            else vs = fminf(vs, val);
+          }
         }
       }
       tc_fence_before();
