@@ -87,6 +87,37 @@ __device__ __forceinline__ double block_sum(double v, MineSmem& sm) {
   return r;
 }
 
+// squared distance of a point row to the staged fp64 seed row (fp64, same
+// operands as the reference's x - x_seed); fp16 rows at d = 128 load as 16
+// independent 16-byte vectors so the whole row is in flight at once
+template <typename T>
+__device__ __forceinline__ double sqdist_seed(const T* a, const double* b, int D) {
+  if constexpr (std::is_same<T, __half>::value) {
+    if (D == 128) {
+      uint4 v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(a) + i);
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const __half* h = reinterpret_cast<const __half*>(&v[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double d = __dsub_rn((double)__half2float(h[e]), b[8 * i + e]);
+          s = fma(d, d, s);
+        }
+      }
+      return s;
+    }
+  }
+  double s = 0.0;
+  for (int c = 0; c < D; ++c) {
+    const double d = __dsub_rn(to_f64(a[c]), b[c]);
+    s = fma(d, d, s);
+  }
+  return s;
+}
+
 template <typename T>
 __device__ __forceinline__ double sqdist_row(const T* a, const T* b, int D) {
   double s = 0.0;
@@ -383,9 +414,10 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
   double vmax; long long imax;
   {
     double bv = -1.0 / 0.0; long long bi = 0x7fffffffffffffffLL;
-    const T* xf = X + first * D;
+    for (int c2 = tid; c2 < D; c2 += MINE_THREADS) sm.cen[c2] = to_f64(X[first * D + c2]);  // seed row (cen is free here)
+    __syncthreads();
     for (int64_t t = tid; t < Tn; t += MINE_THREADS) {
-      double d = sqdist_row(X + t * D, xf, D);
+      double d = sqdist_seed(X + t * D, sm.cen, D);
       near_[t] = d;
       if (d > bv) { bv = d; bi = t; }
     }
@@ -398,10 +430,11 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
     if (n == k) break;
     if (tid == 0) sm.chosen[n] = (int)imax;
     ++n;
-    const T* xn = X + imax * D;
+    for (int c2 = tid; c2 < D; c2 += MINE_THREADS) sm.cen[c2] = to_f64(X[imax * D + c2]);
+    __syncthreads();
     double bv = -1.0 / 0.0; long long bi = 0x7fffffffffffffffLL;
     for (int64_t t = tid; t < Tn; t += MINE_THREADS) {
-      double d = fmin(near_[t], sqdist_row(X + t * D, xn, D));
+      double d = fmin(near_[t], sqdist_seed(X + t * D, sm.cen, D));
       near_[t] = d;
       if (d > bv) { bv = d; bi = t; }
     }
@@ -510,27 +543,68 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
       }
       __syncthreads();
       // ---- centers = sequential fp64 means (numpy axis-0 reduction order) -------
-      for (int i = tid; i < k * D; i += MINE_THREADS) {
-        const int j = i / D, cc = i - j * D;
-        const int n_j = sm.cnt[j];
-        const int* lj = list + sm.off[j];
-        double s = to_f64(X[(int64_t)lj[0] * D + cc]);
-        for (int q = 1; q < n_j; ++q) s = __dadd_rn(s, to_f64(X[(int64_t)lj[q] * D + cc]));
-        sm.cen[j * sm.CST + cc] = __ddiv_rn(s, (double)n_j);
+      // chains (cluster j, channel cc) summed strictly in point order; 8 chains per
+      // thread advance together so their list/X loads are in flight concurrently.
+      // The objective of this round (patterns.py:121) is a second pass over the
+      // same chains against the new means.
+      double part = 0.0;
+      for (int i0 = tid; i0 < k * D; i0 += 8 * MINE_THREADS) {
+        const int* lp[8];
+        int nn[8], ch[8], jj[8];
+        double acc[8];
+        int nmax = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = i0 + e * MINE_THREADS;
+          const bool ok = i < k * D;
+          jj[e] = ok ? i / D : 0;
+          ch[e] = ok ? i - jj[e] * D : 0;
+          nn[e] = ok ? sm.cnt[jj[e]] : 0;
+          lp[e] = list + sm.off[jj[e]];
+          acc[e] = nn[e] > 0 ? to_f64(X[(int64_t)lp[e][0] * D + ch[e]]) : 0.0;
+          nmax = max(nmax, nn[e]);
+        }
+        for (int q = 1; q < nmax; ++q) {
+          double xv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xv[e] = q < nn[e] ? to_f64(X[(int64_t)lp[e][q] * D + ch[e]]) : 0.0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (q < nn[e]) acc[e] = __dadd_rn(acc[e], xv[e]);
+        }
+        double mean[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          mean[e] = nn[e] > 0 ? __ddiv_rn(acc[e], (double)nn[e]) : 0.0;
+          if (nn[e] > 0) sm.cen[jj[e] * sm.CST + ch[e]] = mean[e];
+        }
+        for (int q = 0; q < nmax; ++q) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (q < nn[e]) {
+              const double d = __dsub_rn(to_f64(X[(int64_t)lp[e][q] * D + ch[e]]), mean[e]);
+              part = fma(d, d, part);
+            }
+          }
+        }
       }
       __syncthreads();
-      // ---- objective of this round fused with the next assignment ----------------
-      double part = TC ? assign_tc(Tn, k, sm, lab, lab2, true, tmap, (int64_t)u * Tn, gtile)
-                       : assign_pass(X, Tn, D, k, sm, lab, lab2, near_, true);
-      own_valid = !TC;
       const double obj = block_sum(part, sm);
       if (tid == 0) hist[it] = obj;
       iters = it + 1;
       if (obj == 0.0 || (isfinite(prev) && prev - obj < 1e-6 * prev)) break;
       prev = obj;
       if (it + 1 == 25) break;  // keep the labels the final centers were built from
+      // ---- next assignment --------------------------------------------------------------
+      if (TC) {
+        assign_tc(Tn, k, sm, nullptr, lab2, true, tmap, (int64_t)u * Tn, gtile);
+        own_valid = false;
+      } else {
+        assign_pass(X, Tn, D, k, sm, nullptr, lab2, near_, true);
+        own_valid = true;
+        double* to = own; own = near_; near_ = to;
+      }
       int* tl = lab; lab = lab2; lab2 = tl;
-      double* to = own; own = near_; near_ = to;
     }
     n = k;
   }

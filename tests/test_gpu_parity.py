@@ -242,3 +242,36 @@ def test_tcgen05_mining_matches_cuda_core_and_oracle(pkv, k, monkeypatch):
         np.testing.assert_allclose(tabs["tc"][0][u, :len(cen)], cen, rtol=0, atol=1e-12)
         assert int(tabs["tc"][2][u]) == len(hist)
         np.testing.assert_allclose(tabs["tc"][1][u, :len(hist)], hist, rtol=1e-12)
+
+
+def test_long_decode_pattern_growth_vs_oracle(pkv):
+    """Append-and-refresh far past the pruned-matcher range: the tables grow from 8 to
+    8 + 75 patterns per side (brute-force matcher above 64, shared-W attention path),
+    codes/indices stay bit-exact vs the oracle replay and attention stays within 1e-3."""
+    from paper_2510_05176_b200.config import EngineConfig
+    from paper_2510_05176_b200.export import export_unit
+
+    d, tp, G = 64, 256, 64
+    steps = 75 * G + 10
+    k, v = O.synth_unit(O.unit_seed(5, 5, 5), tp + steps, d)
+    k = k.astype(np.float16).astype(np.float64)
+    v = v.astype(np.float16).astype(np.float64)
+    cfg = dict(bits=2, pattern_count=8, group_size=G, residual_window=G)
+    cache = pkv.PatternKVCache(EngineConfig(**cfg), 1, d, dtype=torch.float16, max_tokens=512)
+    kt = torch.from_numpy(k).half().cuda()
+    vt = torch.from_numpy(v).half().cuda()
+    cache.prefill(kt[None, :tp], vt[None, :tp])
+    for t in range(tp, tp + steps):
+        cache.append(kt[None, t], vt[None, t])
+    h = O.replay(k[:tp], v[:tp], k[tp:], v[tp:], O.Knobs(**cfg))
+    st = export_unit(cache, 0, with_bytes=False)
+    assert len(st.kpat) == len(h.kpat) == 8 + 75
+    np.testing.assert_array_equal(st.kpat, h.kpat)
+    np.testing.assert_array_equal(st.k_idx, np.concatenate([b[5] for b in h.k_blocks]))
+    np.testing.assert_array_equal(st.k_codes, np.concatenate([b[4] for b in h.k_blocks]))
+    np.testing.assert_array_equal(st.v_idx, np.array([x[3] for x in h.v_tok]))
+    np.testing.assert_array_equal(st.v_codes, np.stack([x[2] for x in h.v_tok]))
+    q = np.random.default_rng(9).normal(size=(1, 4, d)).astype(np.float32)
+    out = cache.decode_attention(torch.from_numpy(q).cuda()).cpu().numpy()
+    ref = O.head_attention(h, q[0].astype(np.float64), 1.0 / math.sqrt(d))
+    assert np.abs(out[0] - ref).max() / np.abs(ref).max() <= 1e-3
