@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpkv_b200.so")
-SOURCES = ["pkv_encode.cu", "pkv_mine.cu", "pkv_attn.cu", "pkv_misc.cu", "pkv_capi.cu"]
+SOURCES = ["pkv_encode.cu", "pkv_encode_tc.cu", "pkv_mine.cu", "pkv_attn.cu", "pkv_misc.cu", "pkv_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -25,7 +25,7 @@ FLAGS = [
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "pkv_common.cuh"),
+    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "pkv_common.cuh"), os.path.join(CSRC, "pkv_sm100.cuh"),
             os.path.join(HERE, "..", "include", "pkv.h")]
     if os.path.exists(obj) and all(os.path.getmtime(obj) >= os.path.getmtime(d) for d in deps):
         return obj

@@ -357,6 +357,7 @@ extern "C" int pkv_cache_buffer(pkv_cache* c, const char* name, void** ptr, int6
       {"kcodes", d.kcodes, U * NB * d.blk_bytes}, {"vcodes", d.vcodes, U * NB * d.blk_bytes},
       {"kparam32", d.kparam32, U * NB * 2 * d.Dp * 4}, {"vparam32", d.vparam32, U * NB * d.GP * 8},
       {"kpat32", d.kpat32, U * P * d.Dp * 4}, {"vpat32", d.vpat32, U * P * d.Dp * 4},
+      {"stats", c->stats, c->stats ? 16 : 0},
   };
   for (auto& e : tab) {
     if (std::strcmp(e.n, name) == 0) {
@@ -561,7 +562,14 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
     using T_ = std::remove_pointer_t<decltype(tp)>;
     SpanSrc<T_> sk{(const T_*)k, T * c->D, 0, INT64_MAX / 4};
     SpanSrc<T_> sv{(const T_*)v, T * c->D, 0, INT64_MAX / 4};
-    cudaError_t e1 = launch_encode<T_>(c->dev, sk, sv, 0, c->nb, st);
+    cudaError_t e1 = cudaErrorNotSupported;
+    if constexpr (std::is_same<T_, __half>::value)
+      e1 = launch_encode_tc(c->dev, std::max(c->pk_bound, c->pv_bound), (const __half*)k, (const __half*)v, T,
+                            T * c->D, 0, c->nb, st);
+    if (e1 == cudaErrorNotSupported) {
+      (void)cudaGetLastError();
+      e1 = launch_encode<T_>(c->dev, sk, sv, 0, c->nb, st);
+    }
     if (e1 != cudaSuccess) return e1;
     // window = newest min(T, W) rows (engine.py:166-167)
     const size_t off = (size_t)commit_n * c->D;
