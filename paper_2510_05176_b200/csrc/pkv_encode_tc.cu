@@ -43,8 +43,6 @@ using namespace sm100;
 constexpr int NTHR = 512;   // 16 warps: 0-7 K pipeline, 8-15 V pipeline
 constexpr int GT = 256;     // threads per side group
 constexpr int PM = 32;      // max patterns per side on this path
-constexpr int MR = 144;     // permuted fp32 pattern row: 4 lane segments of 36 floats (bank skew)
-constexpr int RS = 136;     // K residual tile row stride (floats): conflict-free float2 columns
 constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23
 #define FE_INF __int_as_float(0x7f800000)
 #define FE_NAN __int_as_float(0x7fc00000)
@@ -54,46 +52,54 @@ constexpr float TWO_M17 = 7.62939453125e-06f;
 constexpr float TWO_M22 = 2.384185791015625e-07f;
 
 // ---- shared memory map (bytes from a 1024-aligned base) ---------------------------------
-constexpr int SZ_X = 32768;                       // one side's span tile [2 halves][128 rows][128 B]
-constexpr int OFF_X = 0;                          // X[side]
+// Four 4-warp subgroups: K0, K1 (warps 0-7) and V0, V1 (warps 8-15); the two subgroups of
+// a side alternate over the items of each unit and share that side's pattern tables.
+constexpr int SZ_X = 32768;                       // span tile [2 halves][128 rows][128 B], SW128
+constexpr int OFF_X = 0;                          // X[sgi], sgi = 2*side + sg
 constexpr int SZ_B = 16384;                       // centered hi [2][32][128 B] then lo [2][32][128 B]
-constexpr int OFF_B = OFF_X + 2 * SZ_X;
-constexpr int SZ_M = PM * MR * 4;                 // permuted fp32 table
-constexpr int OFF_M = OFF_B + 2 * SZ_B;
-constexpr int OFF_R = OFF_M + 2 * SZ_M;           // K residual tile [128][RS] f32
-constexpr int OFF_KW = OFF_R + 128 * RS * 4;      // K code words [8 tiles][32 lanes][<= 8]
-constexpr int OFF_TOK = OFF_KW + 8 * 32 * 8 * 4;  // per side: guess, cand, dg, xabs, fidx, ed
-constexpr int SZ_TOK = 6 * 128 * 4;
-constexpr int OFF_PAT = OFF_TOK + 2 * SZ_TOK;     // per side: bb, mn, pm, mabsr [4][32], mabsc[128], flags[4]
-constexpr int SZ_PAT = (4 * 32 + 128 + 4) * 4;
-constexpr int OFF_KQ = OFF_PAT + 2 * SZ_PAT;     // K per-channel exact params: lo64[128], scale64[128]
-constexpr int OFF_BAR = OFF_KQ + 2 * 128 * 8;     // xfull[2], mma[2] (8 B each) + tmem addr
-constexpr int SMEM_BYTES = OFF_BAR + 64 + 1024;   // + alignment slack
+constexpr int OFF_B = OFF_X + 4 * SZ_X;           // B[side]
+constexpr int SZ_M = PM * 128 * 4;                // fp32 table, lane-permuted rows (mslot)
+constexpr int OFF_M = OFF_B + 2 * SZ_B;           // M[side]
+constexpr int NSC = 9;                            // scratch arrays of 128 words per subgroup
+constexpr int SZ_SC = NSC * 128 * 4;
+constexpr int OFF_SC = OFF_M + 2 * SZ_M;          // SC[sgi]
+constexpr int SZ_PAT = (4 * 32 + 128 + 4) * 4;    // bb, mn, pm, mabsr [4][32], mabsc[128], flags[4]
+constexpr int OFF_PAT = OFF_SC + 4 * SZ_SC;       // PAT[side]
+constexpr int OFF_BAR = OFF_PAT + 2 * SZ_PAT;     // xfull[4], mma[4], release counters[4], tmem addr
+constexpr int OFF_KW = OFF_BAR + 128;             // 2-bit K code words [2][8 tiles][32 lanes][4]
+constexpr int SZ_KW = 8 * 32 * 4 * 4;
+__host__ __device__ constexpr int smem_bytes(int bits) { return OFF_KW + (bits == 2 ? 2 * SZ_KW : 0) + 1024; }
+static_assert(smem_bytes(2) <= 232448 && smem_bytes(4) <= 232448, "shared memory budget");
 
-struct Tok {
-  int* guess; uint32_t* cand; float* dg; float* xabs; int* fidx; float* ed;
-  __device__ Tok(unsigned char* sb, int side) {
-    unsigned char* p = sb + OFF_TOK + side * SZ_TOK;
-    guess = reinterpret_cast<int*>(p);
-    cand = reinterpret_cast<uint32_t*>(p + 512);
-    dg = reinterpret_cast<float*>(p + 1024);
-    xabs = reinterpret_cast<float*>(p + 1536);
-    fidx = reinterpret_cast<int*>(p + 2048);
-    ed = reinterpret_cast<float*>(p + 2560);
-  }
+// per-subgroup scratch: token arrays (index t) during the token stage, then per-group arrays
+// (index = token for V, channel for K) for the scalar pass
+#define SMEM_PTR(p) __builtin_assume(__isShared(p))
+struct Scr {   // per-subgroup scratch, 9 arrays of 128 words
+  unsigned char* base;
+  __device__ explicit Scr(unsigned char* sb, int sgi) : base(sb + OFF_SC + sgi * SZ_SC) {}
+  __device__ int* guess() const { return reinterpret_cast<int*>(base); }             // token stage
+  __device__ float* lo32() const { return reinterpret_cast<float*>(base); }          // scalar pass (alias)
+  __device__ uint32_t* cand() const { return reinterpret_cast<uint32_t*>(base + 512); }
+  __device__ float* inv() const { return reinterpret_cast<float*>(base + 512); }     // scalar pass (alias)
+  __device__ float* hg() const { return reinterpret_cast<float*>(base + 1024); }     // 1/2 - guard
+  __device__ float* kmx() const { return reinterpret_cast<float*>(base + 1536); }    // keyed residual max
+  __device__ float* kmn() const { return reinterpret_cast<float*>(base + 2048); }    // keyed residual min
+  __device__ float* xmx() const { return reinterpret_cast<float*>(base + 2560); }    // x max (token)
+  __device__ float* xmn() const { return reinterpret_cast<float*>(base + 3072); }    // x min (token)
+  __device__ int* fidx() const { return reinterpret_cast<int*>(base + 3584); }       // final pattern per token
+  // bit 0 unique extrema (bits 1-7 / 8-14 arg-max / arg-min), bit 1<<16 exact fp64 extrema stored
+  // in (kmx, xmx) / (kmn, xmn) as double halves (K), bit 15 flatten (V)
+  __device__ int* info() const { return reinterpret_cast<int*>(base + 4096); }
 };
-struct Pat {
-  float* bb;     // ||m'_p||^2 (+inf for p >= P)
-  float* mn;     // ||m'_p||
-  float* pm;     // m_a - m_b at the probe channels
-  float* mabsr;  // max_c |m_pc|
-  float* mabsc;  // max_p |m_pc| (K)
-  int* flags;    // [0] P, [1] L2 bound disabled, [2] probe a, [3] probe b
-  __device__ Pat(unsigned char* sb, int side) {
-    float* p = reinterpret_cast<float*>(sb + OFF_PAT + side * SZ_PAT);
-    bb = p; mn = p + 32; pm = p + 64; mabsr = p + 96; mabsc = p + 128;
-    flags = reinterpret_cast<int*>(p + 256);
-  }
+struct Pat {   // per-side pattern scalars
+  unsigned char* base;
+  __device__ explicit Pat(unsigned char* sb, int side) : base(sb + OFF_PAT + side * SZ_PAT) {}
+  __device__ float* bb() const { return reinterpret_cast<float*>(base); }            // ||m'_p||^2 (+inf past P)
+  __device__ float* mn() const { return reinterpret_cast<float*>(base + 128); }      // ||m'_p||
+  __device__ float* pm() const { return reinterpret_cast<float*>(base + 256); }      // m_a - m_b (probe pair)
+  __device__ float* mabsr() const { return reinterpret_cast<float*>(base + 384); }   // max_c |m_pc|
+  __device__ float* mabsc() const { return reinterpret_cast<float*>(base + 512); }   // max_p |m_pc| (K)
+  __device__ int* flags() const { return reinterpret_cast<int*>(base + 1024); }      // P, no-L2, probe a, b
 };
 
 struct Args {
@@ -106,12 +112,19 @@ struct Args {
   double yq;             // RN(1 / qmax)
 };
 
-__device__ __forceinline__ void bar_group(int g) { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(GT) : "memory"); }
+__device__ __forceinline__ void bar_side(int side) { asm volatile("bar.sync %0, %1;" ::"r"(1 + side), "n"(256) : "memory"); }
+__device__ __forceinline__ void bar_sub(int sgi) { asm volatile("bar.sync %0, %1;" ::"r"(3 + sgi), "n"(128) : "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
                : "r"(addr));
+}
+// an .aligned warp instruction: tells ptxas the warp is converged here, so the shuffles that
+// follow in an out-of-line function need no divergence-tolerant (WARPSYNC.COLLECTIVE) copies
+__device__ __forceinline__ void warp_converged() {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(0u));
 }
 __device__ __forceinline__ uint32_t movm_t(uint32_t a) {
   uint32_t d;
@@ -148,11 +161,13 @@ __device__ __forceinline__ float xt_at(const unsigned char* xt, int row, int ch)
   const unsigned char* p = xt + h * 16384 + row * 128 + ((((c >> 3) ^ (row & 7)) << 4) | ((c & 7) << 1));
   return __half2float(*reinterpret_cast<const __half*>(p));
 }
-// position of channel c in a permuted fp32 pattern row: lane q's 32 channels
-// (16j + 8hc + 2q + e) are contiguous at q*36 + 4j + 2hc + e
-__device__ __forceinline__ int mpos(int c) {
+// fp32 pattern row p, lane-permuted: lane q's 32 channels (16j + 8hc + 2q + e) form segment
+// q; chunk j (channels 16j + {0,1,8,9} + 2q) sits at slot j ^ 2q ^ (p & 1), so the four
+// lanes of a row read distinct bank groups (and rows of different parity interleave)
+__device__ __forceinline__ int mslot(int p, int q, int j) { return q * 32 + 4 * ((j ^ (2 * q) ^ (p & 1)) & 7); }
+__device__ __forceinline__ int mpos(int p, int c) {
   const int j = c >> 4, hc = (c >> 3) & 1, q = (c >> 1) & 3, e = c & 1;
-  return q * 36 + 4 * j + 2 * hc + e;
+  return mslot(p, q, j) + 2 * hc + e;
 }
 
 // exact division by the integer qmax (Markstein: y = RN(1/b), q0 = RN(a y),
@@ -225,6 +240,8 @@ __device__ __forceinline__ bool gate_le(double flat, double raw, double thr) {
 // fp64 re-match of token row t over the whole table (patterns.py:217-221): lane q of the
 // row's quad takes patterns p = q (mod 4); lowest index on ties.  Whole warp calls.
 __device__ __noinline__ int refine64(const unsigned char* X, int t, const double* p64, int P, int q) {
+  SMEM_PTR(X);
+  warp_converged();
   double bv = __longlong_as_double(0x7ff0000000000000LL);
   int bi = 0x7fffffff;
   for (int p = q; p < P; p += 4) {
@@ -247,63 +264,6 @@ __device__ __noinline__ int refine64(const unsigned char* X, int t, const double
   }
   return bi;
 }
-// lane-local keyed extrema of the residual of rows g (+8) against pattern rows p0, p1
-// (same arithmetic and keys as resid_pass)
-__device__ __noinline__ void cand_stats(const unsigned char* X, const float* M, int gw, int lane, int p0, int p1,
-                                        float* out) {
-  const int g = lane >> 2, q = lane & 3;
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    const int t = 16 * gw + g + 8 * h;
-    const float* mr = M + (h ? p1 : p0) * MR + q * 36;
-    float mx = -FE_INF, mn = FE_INF;
-#pragma unroll 4
-    for (int e = 0; e < 32; ++e) {
-      const int j = e >> 2, k = e & 3;
-      const int ch = 16 * j + 8 * (k >> 1) + 2 * q + (k & 1);
-      const float key = fkey(__fsub_rn(xt_at(X, t, ch), mr[e]), (uint32_t)e, 0xffffffe0u);
-      mx = fmaxf(mx, key);
-      mn = fminf(mn, key);
-    }
-    out[2 * h] = mx;
-    out[2 * h + 1] = mn;
-  }
-}
-// V row: lane-local fp64 extrema over the elements whose key lies in the error window
-__device__ __noinline__ void v_slow_extrema(const __half* xrow, const double* mrow, const float* mr32, int q,
-                                            float hib, float lob, double* omx, double* omn) {
-  double dmx = -__longlong_as_double(0x7ff0000000000000LL), dmn = -dmx;
-  for (int e = 0; e < 32; ++e) {
-    const int j = e >> 2, k = e & 3;
-    const int ch = 16 * j + 8 * (k >> 1) + 2 * q + (k & 1);
-    const float xv = __half2float(xrow[ch]);
-    const float key = fkey(__fsub_rn(xv, mr32[e]), (uint32_t)e, 0xffffffe0u);
-    if (key >= hib || key <= lob) {
-      const double v64 = __dsub_rn((double)xv, mrow[ch]);
-      if (key >= hib) dmx = fmax(dmx, v64);
-      if (key <= lob) dmn = fmin(dmn, v64);
-    }
-  }
-  *omx = dmx;
-  *omn = dmn;
-}
-// K channel: lane-local fp64 extrema over its 16 tokens whose key lies in the window
-__device__ __noinline__ void k_slow_extrema(const float* R, const int* fidx, const __half* xsrc, const double* p64,
-                                            int ch, int g, float hib, float lob, double* omx, double* omn) {
-  double dmx = -__longlong_as_double(0x7ff0000000000000LL), dmn = -dmx;
-  for (int e = 0; e < 16; ++e) {
-    const int tt = e >> 1, h = e & 1, t = 16 * tt + 8 * h + g;
-    const float key = fkey(R[t * RS + ch], (uint32_t)e, 0xfffffff0u);
-    if (key >= hib || key <= lob) {
-      const double v64 = __dsub_rn((double)__half2float(xsrc[(int64_t)t * 128 + ch]), p64[(int64_t)fidx[t] * 128 + ch]);
-      if (key >= hib) dmx = fmax(dmx, v64);
-      if (key <= lob) dmn = fmin(dmn, v64);
-    }
-  }
-  *omx = dmx;
-  *omn = dmn;
-}
-
 // ---------------------------------------------------------------------------------------
 // pattern staging for (unit u, side): permuted fp32 table, centered hi/lo B operand,
 // per-pattern scalars.  Called by the side group between group barriers.
@@ -317,19 +277,20 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
   unsigned char* B = sb + OFF_B + side * SZ_B;
   Pat pt(sb, side);
   const int pa = c.probe[((int64_t)u * 2 + side) * 16 + 0], pbc = c.probe[((int64_t)u * 2 + side) * 16 + 1];
-  if (gtid == 0) pt.flags[1] = 0;
+  if (gtid == 0) pt.flags()[1] = 0;
   for (int i = gtid; i < PM * 128; i += GT) {
     const int p = i >> 7, ch = i & 127;
-    M[p * MR + mpos(ch)] = p < P ? p32[(int64_t)p * c.Dp + ch] : 0.f;
+    M[p * 128 + mpos(p, ch)] = p < P ? p32[(int64_t)p * c.Dp + ch] : 0.f;
   }
   if (side == 0 && gtid < 128) {
     float m = 0.f;
     for (int p = 0; p < P; ++p) m = fmaxf(m, fabsf(p32[(int64_t)p * c.Dp + gtid]));
-    pt.mabsc[gtid] = m;
+    pt.mabsc()[gtid] = m;
   }
-  bar_group(side);  // flags[1] reset visible
+  bar_side(side);  // flags[1] reset visible
   // one warp per pattern (8 warps x 4): mean in fp64, centered hi/lo fp16 rows
   const int w = gtid >> 5, lane = gtid & 31;
+  warp_converged();
   for (int p = w; p < PM; p += 8) {
     double mv[4], s = 0.0;
     float amax = 0.f;
@@ -358,38 +319,40 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
     }
     ss = warp_sum_dd(ss);
     amax = warp_max_f(amax);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&pt.flags[1], 1);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&pt.flags()[1], 1);
     if (lane == 0) {
-      pt.bb[p] = p < P ? (float)ss : FE_INF;
-      pt.mn[p] = p < P ? (float)sqrt(ss) : 0.f;
-      pt.pm[p] = p < P ? (float)__dsub_rn(p64[(int64_t)p * 128 + pa], p64[(int64_t)p * 128 + pbc]) : 0.f;
-      pt.mabsr[p] = amax;
+      pt.bb()[p] = p < P ? (float)ss : FE_INF;
+      pt.mn()[p] = p < P ? (float)sqrt(ss) : 0.f;
+      pt.pm()[p] = p < P ? (float)__dsub_rn(p64[(int64_t)p * 128 + pa], p64[(int64_t)p * 128 + pbc]) : 0.f;
+      pt.mabsr()[p] = amax;
     }
   }
   if (gtid == 0) {
-    pt.flags[0] = P;
-    pt.flags[2] = pa;
-    pt.flags[3] = pbc;
+    pt.flags()[0] = P;
+    pt.flags()[2] = pa;
+    pt.flags()[3] = pbc;
   }
   fence_proxy_async();  // generic-proxy writes of B -> tensor-core reads
 }
 
 // ---------------------------------------------------------------------------------------
-// residual pass of one warp over its 16 tokens (rows g, g+8) against pattern rows
-// idx[0], idx[1]: r = x - m in fragment layout, keyed extrema, x extrema
+// residual pass of one warp over a 16-token tile (rows tb + g, tb + g + 8) against pattern
+// rows idx[0], idx[1]: r = x - m in mma-fragment layout, keyed extrema, x extrema
 // ---------------------------------------------------------------------------------------
 struct RowStats {
   float kmx[2], kmn[2];   // lane-local keyed extrema of r (5-bit element index)
   float xmx[2], xmn[2];   // lane-local extrema of x
 };
-__device__ __forceinline__ void resid_pass(const unsigned char* X, const float* M, int gw, int lane, const int idx[2],
+template <bool STORE>
+__device__ __forceinline__ void resid_tile(const unsigned char* X, const float* M, int tb, int lane, const int idx[2],
                                            float (&r)[2][8][4], RowStats& st) {
   const int q = lane & 3;
   const uint32_t xbase = smem_u32(X);
-  const int lrow = 16 * gw + (lane & 7) + 8 * ((lane >> 3) & 1);
+  const int lrow = tb + (lane & 7) + 8 * ((lane >> 3) & 1);
   const int lchk = lane >> 4;
-  const float* m0p = M + idx[0] * MR + q * 36;
-  const float* m1p = M + idx[1] * MR + q * 36;
+  const float* m0p = M + idx[0] * 128 + q * 32;
+  const float* m1p = M + idx[1] * 128 + q * 32;
+  const int sw0 = (2 * q) ^ (idx[0] & 1), sw1 = (2 * q) ^ (idx[1] & 1);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     st.kmx[h] = -FE_INF; st.kmn[h] = FE_INF; st.xmx[h] = -FE_INF; st.xmn[h] = FE_INF;
@@ -399,24 +362,58 @@ __device__ __forceinline__ void resid_pass(const unsigned char* X, const float* 
     uint32_t a0, a1, a2, a3;
     const uint32_t addr = xbase + (j >> 2) * 16384 + lrow * 128 + ((((2 * (j & 3) + lchk) ^ (lrow & 7))) << 4);
     ldsm_x4(addr, a0, a1, a2, a3);
-    const float4 m0 = *reinterpret_cast<const float4*>(m0p + 4 * j);
-    const float4 m1 = *reinterpret_cast<const float4*>(m1p + 4 * j);
+    const float4 m0 = *reinterpret_cast<const float4*>(m0p + 4 * (j ^ sw0));
+    const float4 m1 = *reinterpret_cast<const float4*>(m1p + 4 * (j ^ sw1));
     const float x0[4] = {h2f_lo(a0), h2f_hi(a0), h2f_lo(a2), h2f_hi(a2)};
     const float x1[4] = {h2f_lo(a1), h2f_hi(a1), h2f_lo(a3), h2f_hi(a3)};
-    r[0][j][0] = __fsub_rn(x0[0], m0.x); r[0][j][1] = __fsub_rn(x0[1], m0.y);
-    r[0][j][2] = __fsub_rn(x0[2], m0.z); r[0][j][3] = __fsub_rn(x0[3], m0.w);
-    r[1][j][0] = __fsub_rn(x1[0], m1.x); r[1][j][1] = __fsub_rn(x1[1], m1.y);
-    r[1][j][2] = __fsub_rn(x1[2], m1.z); r[1][j][3] = __fsub_rn(x1[3], m1.w);
+    const float rv[2][4] = {{__fsub_rn(x0[0], m0.x), __fsub_rn(x0[1], m0.y), __fsub_rn(x0[2], m0.z), __fsub_rn(x0[3], m0.w)},
+                            {__fsub_rn(x1[0], m1.x), __fsub_rn(x1[1], m1.y), __fsub_rn(x1[2], m1.z), __fsub_rn(x1[3], m1.w)}};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      if constexpr (STORE) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r[h][j][e] = rv[h][e];
+      }
       const float* xx = h ? x1 : x0;
-      const float k0 = fkey(r[h][j][0], 4 * j + 0, 0xffffffe0u), k1 = fkey(r[h][j][1], 4 * j + 1, 0xffffffe0u);
-      const float k2 = fkey(r[h][j][2], 4 * j + 2, 0xffffffe0u), k3 = fkey(r[h][j][3], 4 * j + 3, 0xffffffe0u);
+      const float k0 = fkey(rv[h][0], 4 * j + 0, 0xffffffe0u), k1 = fkey(rv[h][1], 4 * j + 1, 0xffffffe0u);
+      const float k2 = fkey(rv[h][2], 4 * j + 2, 0xffffffe0u), k3 = fkey(rv[h][3], 4 * j + 3, 0xffffffe0u);
       st.kmx[h] = fmax3(st.kmx[h], k0, k1); st.kmx[h] = fmax3(st.kmx[h], k2, k3);
       st.kmn[h] = fmin3(st.kmn[h], k0, k1); st.kmn[h] = fmin3(st.kmn[h], k2, k3);
       st.xmx[h] = fmax3(st.xmx[h], xx[0], xx[1]); st.xmx[h] = fmax3(st.xmx[h], xx[2], xx[3]);
       st.xmn[h] = fmin3(st.xmn[h], xx[0], xx[1]); st.xmn[h] = fmin3(st.xmn[h], xx[2], xx[3]);
     }
+  }
+}
+
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& a0, uint32_t& a1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(a0), "=r"(a1) : "r"(addr));
+}
+// one 8-token row-set (rows tb + g) of a tile against pattern row p: r in fragment layout
+// (channels 16j + 8hc + 2q + e at r[j][2hc + e]), keyed extrema, x extrema
+__device__ __forceinline__ void resid_row(const unsigned char* X, const float* M, int tb, int lane, int p,
+                                          float (&r)[8][4], float& kmx, float& kmn, float& xmx, float& xmn) {
+  const int q = lane & 3;
+  const uint32_t xbase = smem_u32(X);
+  // x2: matrices (rows 0-7, ch lo 8) and (rows 0-7, ch hi 8) of a 16-channel block
+  const int lrow = tb + (lane & 7);
+  const int lchk = (lane >> 3) & 1;
+  const float* mp = M + p * 128 + q * 32;
+  const int sw = (2 * q) ^ (p & 1);
+  kmx = -FE_INF; kmn = FE_INF; xmx = -FE_INF; xmn = FE_INF;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t a0, a1;
+    ldsm_x2(xbase + (j >> 2) * 16384 + lrow * 128 + ((((2 * (j & 3) + lchk) ^ (lrow & 7))) << 4), a0, a1);
+    const float4 m = *reinterpret_cast<const float4*>(mp + 4 * (j ^ sw));
+    const float x[4] = {h2f_lo(a0), h2f_hi(a0), h2f_lo(a1), h2f_hi(a1)};
+    r[j][0] = __fsub_rn(x[0], m.x); r[j][1] = __fsub_rn(x[1], m.y);
+    r[j][2] = __fsub_rn(x[2], m.z); r[j][3] = __fsub_rn(x[3], m.w);
+    const float k0 = fkey(r[j][0], 4 * j + 0, 0xffffffe0u), k1 = fkey(r[j][1], 4 * j + 1, 0xffffffe0u);
+    const float k2 = fkey(r[j][2], 4 * j + 2, 0xffffffe0u), k3 = fkey(r[j][3], 4 * j + 3, 0xffffffe0u);
+    kmx = fmax3(kmx, k0, k1); kmx = fmax3(kmx, k2, k3);
+    kmn = fmin3(kmn, k0, k1); kmn = fmin3(kmn, k2, k3);
+    xmx = fmax3(xmx, x[0], x[1]); xmx = fmax3(xmx, x[2], x[3]);
+    xmn = fmin3(xmn, x[0], x[1]); xmn = fmin3(xmn, x[2], x[3]);
   }
 }
 __device__ __forceinline__ float qmax4(float v) {
@@ -433,492 +430,741 @@ __device__ __forceinline__ float derr(float kmx, float kmn, float M) {
   return 7.62939453125e-06f * (fabsf(kmx) + fabsf(kmn)) + 4.76837158203125e-07f * M;
 }
 
+// ---- rare paths (out of line) -----------------------------------------------------------
+// lane-local keyed extrema of a tile's two rows against candidate pattern rows
+__device__ __noinline__ void cand_stats(const unsigned char* X, const float* M, int tb, int lane, int p0, int p1,
+                                        float* out) {
+  SMEM_PTR(X); SMEM_PTR(M);
+  float r[2][8][4];
+  RowStats st;
+  const int idx[2] = {p0, p1};
+  resid_tile<false>(X, M, tb, lane, idx, r, st);
+  out[0] = st.kmx[0]; out[1] = st.kmn[0]; out[2] = st.kmx[1]; out[3] = st.kmn[1];
+}
+// fp64 extrema of V row t over the elements whose key (fragment-layout index) lies in the
+// error window -- same fp32 arithmetic and keys as resid_tile, one thread
+__device__ __noinline__ void v_exact_slow(const unsigned char* X, const float* M, int t, int p, const double* mrow,
+                                          float hib, float lob, double* hi, double* lo) {
+  SMEM_PTR(X); SMEM_PTR(M);
+  double dmx = -__longlong_as_double(0x7ff0000000000000LL), dmn = -dmx;
+  for (int ch = 0; ch < 128; ++ch) {
+    const int j = ch >> 4, q = (ch >> 1) & 3, k = 2 * ((ch >> 3) & 1) + (ch & 1);
+    const float xv = xt_at(X, t, ch);
+    const float key = fkey(__fsub_rn(xv, M[p * 128 + mslot(p, q, j) + k]), (uint32_t)(4 * j + k), 0xffffffe0u);
+    if (key >= hib || key <= lob) {
+      const double v64 = __dsub_rn((double)xv, mrow[ch]);
+      if (key >= hib) dmx = fmax(dmx, v64);
+      if (key <= lob) dmn = fmin(dmn, v64);
+    }
+  }
+  *hi = dmx;
+  *lo = dmn;
+}
+// exact code of one element from the stored fp64 params (read back through L2)
+__device__ __noinline__ uint32_t exact_code_p(const __half* xp, const double* mp, const double* par_lo,
+                                              const double* par_scale, int qmax) {
+  return exact_code_at(xp, mp, __ldcg(par_lo), __ldcg(par_scale), qmax);
+}
+
 // ---------------------------------------------------------------------------------------
-// one side's pipeline (SIDE 0 = K on warps 0-7, 1 = V on warps 8-15)
+// B-pass of one 16-token tile against pattern rows idx[]: keyed extrema (and, for V, the
+// count of elements inside the fp32 error window of each extremum plus their owners)
 // ---------------------------------------------------------------------------------------
-template <int BITS, int SIDE>
-__device__ __forceinline__ void run_side(const Args& A, unsigned char* sb, const CUtensorMap* tm, uint32_t tmem_base,
-                                         int64_t i0, int64_t i1) {
-  const DevCache& c = A.c;
+template <bool VS>
+__device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat pt, Scr sc, int tb,
+                                    int lane, int i0, int i1) {
+  SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base);
+  const int g = lane >> 2, q = lane & 3, t0 = tb + g;
+  const int idx[2] = {i0, i1};
+  float r[2][8][4];
+  RowStats st;
+  resid_tile<VS>(X, M, tb, lane, idx, r, st);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float kx = qmax4(st.kmx[h]), kn = qmin4(st.kmn[h]);
+    const float xx = qmax4(st.xmx[h]), xn = qmin4(st.xmn[h]);
+    int inf = 0;
+    if constexpr (VS) {
+      const float Rm = fmaxf(fabsf(kx), fabsf(kn));
+      // |key - r64| <= 2^-18 |r| + 2^-24 |r| + 2^-23 |m|: window of twice that
+      const float tolx = 1.52587890625e-05f * Rm + 4.76837158203125e-07f * pt.mabsr()[idx[h]];
+      const float hib = kx - tolx, lob = kn + tolx;
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float key = fkey(r[h][j][e], 4 * j + e, 0xffffffe0u);
+          cnt += (key >= hib) + (key <= lob);
+        }
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+      const uint32_t gm = 0xfu << (4 * g);
+      const uint32_t bmx = __ballot_sync(0xffffffffu, st.kmx[h] == kx) & gm;
+      const uint32_t bmn = __ballot_sync(0xffffffffu, st.kmn[h] == kn) & gm;
+      if (cnt == 2 && __popc(bmx) == 1 && __popc(bmn) == 1) {
+        const int qx = (__ffs(bmx) - 1) & 3, qn = (__ffs(bmn) - 1) & 3;
+        const uint32_t ix = __float_as_uint(kx) & 31u, in_ = __float_as_uint(kn) & 31u;
+        const int chx = 16 * (int)(ix >> 2) + 8 * (int)((ix >> 1) & 1) + 2 * qx + (int)(ix & 1);
+        const int chn = 16 * (int)(in_ >> 2) + 8 * (int)((in_ >> 1) & 1) + 2 * qn + (int)(in_ & 1);
+        inf = 1 | (chx << 1) | (chn << 8);
+      }
+    }
+    if (q == 0) {
+      const int t = t0 + 8 * h;
+      sc.kmx()[t] = kx; sc.kmn()[t] = kn; sc.xmx()[t] = xx; sc.xmn()[t] = xn;
+      if constexpr (VS) sc.info()[t] = inf;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// token stage of one warp over its 32 tokens (its TMEM lane quarter): guess, exact lower
+// bounds, survivors, fp64 re-match.  Leaves the final pattern index in sc.fidx() and the
+// keyed statistics of the final residual in sc.kmx()/kmn/xmx/xmn(/info).
+// ---------------------------------------------------------------------------------------
+__device__ __noinline__ void token_stage(bool vs, Scr sc, Pat pt, const unsigned char* X, const float* M,
+                                         uint64_t* mmab, uint32_t ph, uint32_t tcol, int w, int lane, int P, float pmx,
+                                         const double* p64, unsigned* stats) {
+  SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base);
+  warp_converged();
+  const int g = lane >> 2, q = lane & 3;
+  const int tt_ = 32 * w + lane;  // this thread's token in stages A/C
+  const uint32_t tl = tcol + ((uint32_t)(32 * w) << 16);
+  // ---- A. guess = argmin_p ||m'_p||^2 - 2 x.m'_p --------------------------------------
+  mbar_wait(mmab, ph);
+  tc_fence_after();
+  float best = FE_INF;
+#pragma unroll
+  for (int p0 = 0; p0 < 32; p0 += 16) {
+    uint32_t v[8], v2[8];
+    tmem_ld8(tl + p0, v);
+    tmem_ld8(tl + p0 + 8, v2);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      best = fminf(best, fkey(__fmaf_rn(-2.f, __uint_as_float(v[i]), pt.bb()[p0 + i]), p0 + i, 0xffffffe0u));
+      best = fminf(best, fkey(__fmaf_rn(-2.f, __uint_as_float(v2[i]), pt.bb()[p0 + 8 + i]), p0 + 8 + i, 0xffffffe0u));
+    }
+  }
+  int guess = (int)(__float_as_uint(best) & 31u);
+  if (guess >= P) guess = 0;
+  const float Cg = best;
+  const float px = __fsub_rn(xt_at(X, tt_, pt.flags()[2]), xt_at(X, tt_, pt.flags()[3]));
+  sc.guess()[tt_] = guess;
+  __syncwarp();
+  // ---- B. keyed residual extrema against the guess, per 16-token tile -----------------
+#pragma unroll 1
+  for (int tile = 0; tile < 2; ++tile) {
+    const int tb = 32 * w + 16 * tile;
+    if (vs) b_tile<true>(X, M, pt, sc, tb, lane, sc.guess()[tb + g], sc.guess()[tb + g + 8]);
+    else b_tile<false>(X, M, pt, sc, tb, lane, sc.guess()[tb + g], sc.guess()[tb + g + 8]);
+  }
+  __syncwarp();
+  // ---- C. prune every other pattern by exact lower bounds (thread per token) ----------
+  {
+    const float kx = sc.kmx()[tt_], kn = sc.kmn()[tt_];
+    const float dg = __fsub_rn(kx, kn), xa = fmaxf(fabsf(sc.xmx()[tt_]), fabsf(sc.xmn()[tt_]));
+    const float T2 = derr(kx, kn, pt.mabsr()[guess]);  // >= |dg - d64(guess)|
+    const float dhi = __fadd_rn(dg, T2) * 1.0000002f;
+    const float dlo = fmaxf(__fsub_rn(dg, T2), 0.f) * 0.9999998f;
+    // Popoviciu: osc^2 >= 4 C / d; C_q >= C'_q - C'_g + C_g, C_g >= osc_g^2 / 2
+    const float theta = __fmaf_rn(32.f * dhi, dhi, -0.5f * dlo * dlo) * 1.000001f;
+    const float kap = TWO_M13 * 11.3137085f * xa;  // 2 x (tensor-core + split error) / ||m'||, ||x|| <= sqrt(d) |x|max
+    const float rhs = theta + Cg + kap * pt.mn()[guess] + TWO_M17 * fabsf(Cg);
+    const bool nol2 = pt.flags()[1] != 0;
+    const float pb = __fadd_rn(dhi, 4.76837158203125e-07f * (xa + pmx));  // probe: 2^-21 (|x| + |m|) rounding
+    uint32_t mask = 0;
+#pragma unroll 1
+    for (int p0 = 0; p0 < 32; p0 += 8) {
+      uint32_t v[8];
+      tmem_ld8(tl + p0, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int p = p0 + i;
+        const float bbp = pt.bb()[p];
+        const float cp = __fmaf_rn(-2.f, __uint_as_float(v[i]), bbp);
+        const float lhs = __fmaf_rn(-TWO_M22, bbp, __fmaf_rn(-kap, pt.mn()[p], __fmaf_rn(-TWO_M17, fabsf(cp), cp)));
+        const bool l2ok = nol2 || !(lhs > rhs);
+        const bool prok = fabsf(__fsub_rn(px, pt.pm()[p])) <= pb;
+        mask |= (uint32_t)(l2ok && prok && p < P) << p;
+      }
+    }
+    tc_fence_before();
+    mask &= ~(1u << guess);
+    sc.cand()[tt_] = mask;
+    if (stats && mask) atomicAdd(&stats[2], (unsigned)__popc(mask));
+  }
+  __syncwarp();
+  // ---- D. survivors: full fp32 distance, top-2 with error bounds, fp64 re-match ---------
+#pragma unroll 1
+  for (int tile = 0; tile < 2; ++tile) {
+    const int tb = 32 * w + 16 * tile, t0 = tb + g;
+    const int gi[2] = {sc.guess()[t0], sc.guess()[t0 + 8]};
+    int idx[2] = {gi[0], gi[1]};
+    uint32_t cm[2] = {sc.cand()[t0], sc.cand()[t0 + 8]};
+    if (__any_sync(0xffffffffu, (cm[0] | cm[1]) != 0)) {
+      float bst[2], bstE[2], low[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float kx = sc.kmx()[t0 + 8 * h], kn = sc.kmn()[t0 + 8 * h];
+        bst[h] = __fsub_rn(kx, kn);
+        bstE[h] = derr(kx, kn, pt.mabsr()[gi[h]]);
+        low[h] = FE_INF;  // min over the other evaluated patterns of d - err
+      }
+      while (__any_sync(0xffffffffu, (cm[0] | cm[1]) != 0)) {
+        int pc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          pc[h] = cm[h] ? __ffs(cm[h]) - 1 : -1;
+          cm[h] &= cm[h] - 1;
+        }
+        float s4[4];
+        cand_stats(X, M, tb, lane, pc[0] >= 0 ? pc[0] : gi[0], pc[1] >= 0 ? pc[1] : gi[1], s4);
+        warp_converged();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float cx = qmax4(s4[2 * h]), cn = qmin4(s4[2 * h + 1]);
+          if (pc[h] >= 0) {
+            const float d = __fsub_rn(cx, cn), e = derr(cx, cn, pt.mabsr()[pc[h]]);
+            if (d < bst[h] || (d == bst[h] && pc[h] < idx[h])) {
+              low[h] = fminf(low[h], bst[h] - bstE[h]);
+              bst[h] = d; bstE[h] = e; idx[h] = pc[h];
+            } else {
+              low[h] = fminf(low[h], d - e);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool amb = low[h] <= bst[h] + bstE[h];
+        if (__any_sync(0xffffffffu, amb)) {
+          const int ri = refine64(X, t0 + 8 * h, p64, P, q);
+          if (amb) {
+            idx[h] = ri;
+            if (stats && q == 0) atomicAdd(&stats[0], 1u);
+          }
+        }
+      }
+      // statistics of the final residual where the winner moved
+      if (__any_sync(0xffffffffu, idx[0] != gi[0] || idx[1] != gi[1])) {
+        if (vs) b_tile<true>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
+        else b_tile<false>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
+      }
+    }
+    if (q == 0) { sc.fidx()[t0] = idx[0]; sc.fidx()[t0 + 8] = idx[1]; }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------------------
+// K: per-channel groups over the span's 128 tokens.  Warp w takes channel chunks 2w, 2w+1;
+// in a chunk lane (g, q) holds channels 16jb + 2q + {0,1,8,9} of tokens 16tt + 8h + g.
+// ---------------------------------------------------------------------------------------
+// r of the lane's 16 tokens x 4 channels of chunk jb (NaN for tokens past the span)
+template <bool FULL>
+__device__ __forceinline__ void k_load(const unsigned char* X, const float* M, const int (&fi)[16], int jb, int g,
+                                       int q, int L, float (&rr)[16][4]) {
+  const int c0 = 16 * jb + 2 * q;
+  const int hsel = (c0 >> 6) * 16384, ck = (c0 & 63) >> 3, cw = (c0 & 7) << 1;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int t = 16 * (e >> 1) + 8 * (e & 1) + g;
+    const unsigned char* rowp = X + hsel + t * 128 + cw;
+    const uint32_t xa = *reinterpret_cast<const uint32_t*>(rowp + ((ck ^ (t & 7)) << 4));
+    const uint32_t xb = *reinterpret_cast<const uint32_t*>(rowp + (((ck + 1) ^ (t & 7)) << 4));
+    const int p = fi[e];
+    const float4 m = *reinterpret_cast<const float4*>(M + p * 128 + mslot(p, q, jb));
+    rr[e][0] = __fsub_rn(h2f_lo(xa), m.x); rr[e][1] = __fsub_rn(h2f_hi(xa), m.y);
+    rr[e][2] = __fsub_rn(h2f_lo(xb), m.z); rr[e][3] = __fsub_rn(h2f_hi(xb), m.w);
+    if (!FULL && t >= L) rr[e][0] = rr[e][1] = rr[e][2] = rr[e][3] = FE_NAN;
+  }
+}
+// K pass of chunk jb: keyed extrema per channel, window counts and unique owners (for the
+// exact fp64 params of the scalar pass) and the codes, from fp32 params of the keyed extrema:
+// their error (2^-19 |r| key precision + fp32 residual error) is inside the guard, so every
+// code outside the guard band equals the reference's; guard-band pairs are returned (bit
+// 2e + pr) for the exact fix-up once the fp64 params exist.  *anyslow: a channel of the chunk
+// has several elements inside the fp32 error window of an extremum (k_slow resolves it).
+template <int BITS, bool FULL>
+__device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, Pat pt, Scr sc, int jb, int lane,
+                                        int L, uint32_t* KW, uint32_t* wreg, int* anyslow) {
+  SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base); SMEM_PTR(KW);
+  warp_converged();
   constexpr int QMAX = (1 << BITS) - 1;
   constexpr int HS = 8 / BITS;
-  constexpr int WL = 128 * BITS / 64;  // words per lane per tile
-  const int gtid = threadIdx.x & (GT - 1), gw = gtid >> 5, lane = gtid & 31, g = lane >> 2, q = lane & 3;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + OFF_BAR);
-  uint64_t* xfull = bars + SIDE;
-  uint64_t* mmab = bars + 2 + SIDE;
-  unsigned char* X = sb + OFF_X + SIDE * SZ_X;
+  const int g = lane >> 2, q = lane & 3;
+  int fi[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) fi[e] = sc.fidx()[16 * (e >> 1) + 8 * (e & 1) + g];
+  float rr[16][4];
+  k_load<FULL>(X, M, fi, jb, g, q, L, rr);
+  // all warp collectives first (no divergent code between them), then the per-channel results
+  float lmx[4], lmn[4], gmx[4], gmn[4], hib[4], lob[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    lmx[kk] = -FE_INF; lmn[kk] = FE_INF;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float key = fkey(rr[e][kk], e, 0xfffffff0u);
+      lmx[kk] = fmaxf(lmx[kk], key);
+      lmn[kk] = fminf(lmn[kk], key);
+    }
+    gmx[kk] = lmx[kk]; gmn[kk] = lmn[kk];
+  }
+#pragma unroll
+  for (int o = 4; o <= 16; o <<= 1)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      gmx[kk] = fmaxf(gmx[kk], __shfl_xor_sync(0xffffffffu, gmx[kk], o));
+      gmn[kk] = fminf(gmn[kk], __shfl_xor_sync(0xffffffffu, gmn[kk], o));
+    }
+  int cnt[4];
+  float qlo[4], qinv[4], qhg[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int ch = 16 * jb + 2 * q + (kk & 1) + 8 * (kk >> 1);
+    const float Rm = fmaxf(fabsf(gmx[kk]), fabsf(gmn[kk])), Mc = pt.mabsc()[ch];
+    // |key - r64| <= 2^-19 |r| + 2^-24 |r| + 2^-23 |m|: window of twice that
+    const float tolx = TWO_M17 * Rm + 4.76837158203125e-07f * Mc;
+    hib[kk] = gmx[kk] - tolx; lob[kk] = gmn[kk] + tolx;
+    cnt[kk] = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float key = fkey(rr[e][kk], e, 0xfffffff0u);
+      cnt[kk] += (key >= hib[kk]) + (key <= lob[kk]);
+    }
+    // fp32 params from the keyed extrema; |y - y_exact| <= inv (3 2^-19 R + 2^-21 (R + M) + 2^-23 span)
+    // + qmax 2^-22 + 2^-24, doubled (K1-TC)
+    const float span = __fsub_rn(gmx[kk], gmn[kk]);
+    qlo[kk] = gmn[kk];
+    if (span > 4.f * (3.814697265625e-06f * Rm + 4.76837158203125e-07f * (Rm + Mc))) {
+      qinv[kk] = (float)QMAX * rcp_approx(span);
+      qhg[kk] = 0.5f - (qinv[kk] * (1.1444091796875e-05f * Rm + 9.5367431640625e-07f * (Rm + Mc) +
+                                    2.384185791015625e-07f * span) +
+                        4.76837158203125e-07f * (float)QMAX + 1.1920928955078125e-07f);
+    } else {  // (nearly) constant group: every code exact
+      qinv[kk] = 0.f;
+      qhg[kk] = -1.f;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o <= 16; o <<= 1)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) cnt[kk] += __shfl_xor_sync(0xffffffffu, cnt[kk], o);
+  const uint32_t qm = 0x11111111u << q;
+  uint32_t bmx[4], bmn[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    bmx[kk] = __ballot_sync(0xffffffffu, lmx[kk] == gmx[kk]) & qm;
+    bmn[kk] = __ballot_sync(0xffffffffu, lmn[kk] == gmn[kk]) & qm;
+  }
+  bool slow = false;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int ch = 16 * jb + 2 * q + (kk & 1) + 8 * (kk >> 1);
+    const bool fast = cnt[kk] == 2 && __popc(bmx[kk]) == 1 && __popc(bmn[kk]) == 1;
+    const int gx = (__ffs(bmx[kk]) - 1) >> 2, gn = (__ffs(bmn[kk]) - 1) >> 2;
+    const uint32_t ix = __float_as_uint(gmx[kk]) & 15u, in_ = __float_as_uint(gmn[kk]) & 15u;
+    const int tx = 16 * (int)(ix >> 1) + 8 * (int)(ix & 1) + gx;
+    const int tn = 16 * (int)(in_ >> 1) + 8 * (int)(in_ & 1) + gn;
+    const int inf = fast ? (1 | (tx << 1) | (tn << 8)) : 0;
+    slow |= !fast;
+    if (g == 0) {
+      sc.kmx()[ch] = gmx[kk]; sc.kmn()[ch] = gmn[kk];
+      sc.info()[ch] = inf;
+    }
+  }
+  *anyslow = __any_sync(0xffffffffu, slow);
+  // codes (pairs of channels c0+{0,1} / c0+{8,9} per token) -> K fragment words
+  const int slot0 = 2 * (jb % HS);
+  const int wbase = 2 * (jb / HS);
+  uint32_t badm = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int t = 16 * (e >> 1) + 8 * (e & 1) + g;
+    bool bad0 = false, bad1 = false;
+    const float z0 = zcode(rr[e][0], qlo[0], qinv[0], qhg[0], bad0);
+    const float z1 = zcode(rr[e][1], qlo[1], qinv[1], qhg[1], bad0);
+    const float z2 = zcode(rr[e][2], qlo[2], qinv[2], qhg[2], bad1);
+    const float z3 = zcode(rr[e][3], qlo[3], qinv[3], qhg[3], bad1);
+    uint32_t p0 = zpair(z0, z1), p1 = zpair(z2, z3);
+    if (!FULL && t >= L) { p0 = 0u; p1 = 0u; bad0 = bad1 = false; }
+    badm |= ((uint32_t)bad0 << (2 * e)) | ((uint32_t)bad1 << (2 * e + 1));
+    const uint32_t part = (p0 << (slot0 * BITS)) | (p1 << ((slot0 + 1) * BITS));
+    if constexpr (BITS == 2) {
+      atomicOr(&KW[((e >> 1) * 32 + lane) * 4 + (((e & 1) + wbase) ^ ((lane >> 3) & 3))], part);
+    } else {
+      wreg[e] |= part;
+    }
+  }
+  return badm;
+}
+// exact fix-up of chunk jb's guard-band pairs (bits of badm) from the stored fp64 params
+template <int BITS>
+__device__ __noinline__ void k_fix(const double* kparam64, const Scr sc, int jb, int lane, uint32_t badm,
+                                   const __half* xsrc, const double* p64, int64_t blk, uint32_t* KW, uint32_t* wreg,
+                                   unsigned* stats) {
+  SMEM_PTR(sc.base); SMEM_PTR(KW);
+  constexpr int QMAX = (1 << BITS) - 1;
+  constexpr int HS = 8 / BITS;
+  const int g = lane >> 2, q = lane & 3;
+  const int c0 = 16 * jb + 2 * q;
+  const int slot0 = 2 * (jb % HS), wbase = 2 * (jb / HS);
+  const double* kp = kparam64 + blk * 256;
+  while (badm) {
+    const int bit = __ffs(badm) - 1;
+    badm &= badm - 1;
+    const int e = bit >> 1, pr = bit & 1;
+    const int t = 16 * (e >> 1) + 8 * (e & 1) + g, ch = c0 + 8 * pr;
+    const double* mrow = p64 + (int64_t)sc.fidx()[t] * 128;
+    const __half* xrow = xsrc + (int64_t)t * 128;
+    const uint32_t pv = exact_code_p(xrow + ch, mrow + ch, kp + 128 + ch, kp + ch, QMAX) |
+                        (exact_code_p(xrow + ch + 1, mrow + ch + 1, kp + 128 + ch + 1, kp + ch + 1, QMAX) << 16);
+    const int sh = (slot0 + pr) * BITS;
+    const uint32_t clr = ~(((uint32_t)QMAX | ((uint32_t)QMAX << 16)) << sh);
+    if constexpr (BITS == 2) {
+      uint32_t* wp = &KW[((e >> 1) * 32 + lane) * 4 + (((e & 1) + wbase) ^ ((lane >> 3) & 3))];
+      atomicAnd(wp, clr);
+      atomicOr(wp, pv << sh);
+    } else {
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) wreg[k2] = k2 == e ? ((wreg[k2] & clr) | (pv << sh)) : wreg[k2];
+    }
+    if (stats) atomicAdd(&stats[1], 1u);
+  }
+}
+// groups of chunk jb with several elements inside the fp32 error window: exact fp64 extrema
+// over the window (the 8 lanes of a channel cooperate), stored as double halves in
+// (kmx, xmx) / (kmn, xmn) with info = 1 << 16
+template <bool FULL>
+__device__ __noinline__ void k_slow(const unsigned char* X, const float* M, Pat pt, Scr sc, int jb, int lane, int L,
+                                    const double* p64, unsigned* stats) {
+  SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base);
+  warp_converged();
+  const int g = lane >> 2, q = lane & 3;
+#pragma unroll 1
+  for (int kk = 0; kk < 4; ++kk) {
+    const int ch = 16 * jb + 2 * q + (kk & 1) + 8 * (kk >> 1);
+    const bool slow = !(sc.info()[ch] & 1);
+    if (__any_sync(0xffffffffu, slow)) {
+      const float gmx = sc.kmx()[ch], gmn = sc.kmn()[ch];
+      const float Rm = fmaxf(fabsf(gmx), fabsf(gmn));
+      const float tolx = TWO_M17 * Rm + 4.76837158203125e-07f * pt.mabsc()[ch];
+      const float hib = gmx - tolx, lob = gmn + tolx;
+      const int jj = ch >> 4, k4 = 2 * ((ch >> 3) & 1) + (ch & 1);
+      double dmx = -__longlong_as_double(0x7ff0000000000000LL), dmn = -dmx;
+#pragma unroll 1
+      for (int e = 0; e < 16; ++e) {
+        const int t = 16 * (e >> 1) + 8 * (e & 1) + g;
+        const int p = sc.fidx()[t];
+        const float xv = xt_at(X, t, ch);
+        const float key = fkey(__fsub_rn(xv, M[p * 128 + mslot(p, q, jj) + k4]), (uint32_t)e, 0xfffffff0u);
+        const bool in = (FULL || t < L) && (key >= hib || key <= lob);
+        const double v64 = in ? __dsub_rn((double)xv, p64[(int64_t)p * 128 + ch]) : 0.0;
+        if (in && key >= hib) dmx = fmax(dmx, v64);
+        if (in && key <= lob) dmn = fmin(dmn, v64);
+      }
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1) {
+        dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+        dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+      }
+      if (slow && g == 0) {
+        sc.kmx()[ch] = __int_as_float(__double2hiint(dmx)); sc.xmx()[ch] = __int_as_float(__double2loint(dmx));
+        sc.kmn()[ch] = __int_as_float(__double2hiint(dmn)); sc.xmn()[ch] = __int_as_float(__double2loint(dmn));
+        sc.info()[ch] = 1 << 16;
+        if (stats) atomicAdd(&stats[3], 1u);
+      }
+    }
+  }
+}
+// K scalar pass: one thread per channel -- exact fp64 extrema, params, fast-path constants
+template <int BITS>
+__device__ __forceinline__ void k_scalar(const Args& A, const unsigned char* X, const float* M, const Pat& pt,
+                                         const Scr& sc, int ch, int L, const double* p64, int64_t blk,
+                                         unsigned* stats) {
+  const DevCache& c = A.c;
+  const float gmx = sc.kmx()[ch], gmn = sc.kmn()[ch];
+  const int inf = sc.info()[ch];
+  const float Rm = fmaxf(fabsf(gmx), fabsf(gmn)), Mc = pt.mabsc()[ch];
+  double hi64, lo64;
+  float R = Rm;
+  if (inf & 1) {
+    const int tx = (inf >> 1) & 127, tn = (inf >> 8) & 127;
+    hi64 = __dsub_rn((double)xt_at(X, tx, ch), p64[(int64_t)sc.fidx()[tx] * 128 + ch]);
+    lo64 = __dsub_rn((double)xt_at(X, tn, ch), p64[(int64_t)sc.fidx()[tn] * 128 + ch]);
+  } else {  // exact extrema from the slow pass (info == 1 << 16)
+    hi64 = __hiloint2double(__float_as_int(gmx), __float_as_int(sc.xmx()[ch]));
+    lo64 = __hiloint2double(__float_as_int(gmn), __float_as_int(sc.xmn()[ch]));
+    R = fmaxf(fabsf((float)hi64), fabsf((float)lo64));
+  }
+  const GroupQ gg = make_group(lo64, hi64, (1 << BITS) - 1, A.yq, R, Mc);
+  sc.lo32()[ch] = gg.lo32; sc.inv()[ch] = gg.inv; sc.hg()[ch] = gg.hg;
+  c.kparam64[blk * 256 + ch] = gg.scale;
+  c.kparam64[blk * 256 + 128 + ch] = gg.lo;
+  c.kparam32[blk * 2 * c.Dp + ch] = (float)gg.scale;
+  c.kparam32[blk * 2 * c.Dp + c.Dp + ch] = (float)gg.lo;
+}
+// ---------------------------------------------------------------------------------------
+// V: per-token groups over channels
+// ---------------------------------------------------------------------------------------
+// scalar pass: one thread per token -- exact fp64 extrema, gate, params, fast-path constants
+template <int BITS>
+__device__ __forceinline__ void v_scalar(const Args& A, const unsigned char* X, const float* M, const Pat& pt,
+                                         const Scr& sc, int t, int L, int64_t start, int u, int64_t blk,
+                                         const double* p64, unsigned* stats) {
+  const DevCache& c = A.c;
+  const int idx = sc.fidx()[t];
+  const float kx = sc.kmx()[t], kn = sc.kmn()[t], xx = sc.xmx()[t], xn = sc.xmn()[t];
+  int inf = sc.info()[t];
+  const float xa = fmaxf(fabsf(xx), fabsf(xn)), Mr = pt.mabsr()[idx];
+  const float Rm = fmaxf(fabsf(kx), fabsf(kn));
+  const double* mrow = p64 + (int64_t)idx * 128;
+  double hi64, lo64;
+  if (inf & 1) {
+    const int chx = (inf >> 1) & 127, chn = (inf >> 8) & 127;
+    hi64 = __dsub_rn((double)xt_at(X, t, chx), mrow[chx]);
+    lo64 = __dsub_rn((double)xt_at(X, t, chn), mrow[chn]);
+  } else {
+    const float tolx = 1.52587890625e-05f * Rm + 4.76837158203125e-07f * Mr;
+    v_exact_slow(X, M, t, idx, mrow, kx - tolx, kn + tolx, &hi64, &lo64);
+    if (stats && t < L) atomicAdd(&stats[3], 1u);
+  }
+  // gate (gate.py:180-188; --no-v-gate flattens, engine.py:235-237)
+  const double raw = __dsub_rn((double)xx, (double)xn);
+  const double flat = __dsub_rn(hi64, lo64);
+  const bool flatten = c.use_vgate ? (raw > 0.0 && gate_le(flat, raw, c.thr)) : true;
+  const GroupQ gq = flatten ? make_group(lo64, hi64, (1 << BITS) - 1, A.yq, Rm, Mr)
+                            : make_group((double)xn, (double)xx, (1 << BITS) - 1, A.yq, xa, 0.f);
+  sc.lo32()[t] = gq.lo32; sc.inv()[t] = gq.inv; sc.hg()[t] = gq.hg;
+  sc.info()[t] = inf | (flatten ? (1 << 15) : 0);
+  if (t < L) {
+    const int64_t tok = (int64_t)u * c.Tcap + start + t;
+    const int64_t slot = blk * c.GP + t;
+    c.vparam64[2 * tok] = gq.scale;
+    c.vparam64[2 * tok + 1] = gq.lo;
+    c.vparam32[2 * slot] = (float)gq.scale;
+    c.vparam32[2 * slot + 1] = (float)gq.lo;
+    c.vidx[slot] = (int16_t)(flatten ? idx : RAW);
+    if (c.keep_diag && c.vdiag) { c.vdiag[2 * tok] = raw; c.vdiag[2 * tok + 1] = flat; }
+  }
+}
+// codes pass of one 8-token row-set (rows rb + g): codes, exact fix-ups, movmatrix to the
+// V^T fragment layout, this row-set's words of the tile
+template <int BITS>
+__device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, int blk_bytes, int64_t Tcap,
+                                     const unsigned char* X, const float* M, Scr sc, int rb, int lane, int L, int u,
+                                     int64_t start, int64_t blk, const __half* xsrc, const double* p64,
+                                     unsigned* stats) {
+  SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(sc.base);
+  constexpr int QMAX = (1 << BITS) - 1;
+  constexpr int HS = 8 / BITS;
+  constexpr int WL = 128 * BITS / 64;
+  const int g = lane >> 2, q = lane & 3;
+  const int t = rb + g, h = (rb >> 3) & 1;
+  const int idx = sc.fidx()[t];
+  const bool flatten = (sc.info()[t] >> 15) & 1;
+  const float lo32 = sc.lo32()[t], inv = sc.inv()[t], hg = sc.hg()[t];
+  float r[8][4];
+  float d0, d1, d2, d3;
+  resid_row(X, M, rb, lane, idx, r, d0, d1, d2, d3);
+  if (!flatten) {  // RAW payload: the exact input row (rare)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) r[j][e] = xt_at(X, t, 16 * j + 8 * (e >> 1) + 2 * q + (e & 1));
+  }
+  uint32_t pp[16];
+  uint32_t badm = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    bool bad0 = false, bad1 = false;
+    const float z0 = zcode(r[j][0], lo32, inv, hg, bad0), z1 = zcode(r[j][1], lo32, inv, hg, bad0);
+    const float z2 = zcode(r[j][2], lo32, inv, hg, bad1), z3 = zcode(r[j][3], lo32, inv, hg, bad1);
+    pp[2 * j] = zpair(z0, z1);
+    pp[2 * j + 1] = zpair(z2, z3);
+    badm |= ((uint32_t)bad0 << (2 * j)) | ((uint32_t)bad1 << (2 * j + 1));
+  }
+  if (t >= L) {
+    badm = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pp[i] = 0u;
+  }
+  if (badm) {  // rare: the reference's fp64 sequence decides inside the guard band
+    const double* mr = flatten ? p64 + (int64_t)idx * 128 : nullptr;
+    const __half* xrow = xsrc + (int64_t)t * 128;
+    const double* vp = vparam64 + 2 * ((int64_t)u * Tcap + start + t);
+#pragma unroll 1
+    while (badm) {
+      const int i = __ffs(badm) - 1;
+      badm &= badm - 1;
+      const int ca = 16 * (i >> 1) + 8 * (i & 1) + 2 * q;
+      const uint32_t pv = exact_code_p(xrow + ca, mr ? mr + ca : nullptr, vp + 1, vp, QMAX) |
+                          (exact_code_p(xrow + ca + 1, mr ? mr + ca + 1 : nullptr, vp + 1, vp, QMAX) << 16);
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) pp[k2] = k2 == i ? pv : pp[k2];
+      if (stats) atomicAdd(&stats[1], 1u);
+    }
+  }
+  uint32_t words[WL / 2];
+#pragma unroll
+  for (int i = 0; i < WL / 2; ++i) words[i] = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t t0v = movm_t(pp[2 * j]), t1v = movm_t(pp[2 * j + 1]);  // hiRow 0 / 1 of sub-tile j
+    const int s0 = 2 * (j % HS);
+    words[j / HS] |= (t0v << (s0 * BITS)) | (t1v << ((s0 + 1) * BITS));
+  }
+  uint32_t* dst = reinterpret_cast<uint32_t*>(vcodes + blk * blk_bytes + (size_t)((rb >> 4) * 32 + lane) * WL * 4);
+#pragma unroll
+  for (int i = 0; i < WL / 2; ++i) dst[h + 2 * i] = words[i];
+}
+
+// ---------------------------------------------------------------------------------------
+// one subgroup (4 warps) of a side: its items of every unit in the CTA's range
+// ---------------------------------------------------------------------------------------
+template <int BITS, int SIDE>
+__device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const CUtensorMap* tm, uint32_t tmem,
+                                        int64_t i0, int64_t i1) {
+  const DevCache& c = A.c;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sg = (warp >> 2) & 1, w = warp & 3, sgi = 2 * SIDE + sg;
+  const int gtid = threadIdx.x & 255, st = 32 * w + lane;
+  unsigned char* X = sb + OFF_X + sgi * SZ_X;
   unsigned char* B = sb + OFF_B + SIDE * SZ_B;
   const float* M = reinterpret_cast<const float*>(sb + OFF_M + SIDE * SZ_M);
-  Tok tk(sb, SIDE);
+  uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW + sg * SZ_KW);
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(sb + OFF_BAR) + sgi;
+  uint64_t* mmab = reinterpret_cast<uint64_t*>(sb + OFF_BAR + 32) + sgi;
+  int* rel = reinterpret_cast<int*>(sb + OFF_BAR + 64) + sgi;
+  Scr sc(sb, sgi);
   Pat pt(sb, SIDE);
-  const __half* src = A.src[SIDE];
+  const int nb = A.nb;
   unsigned* stats = c.stats;
 
+  auto first_item = [&](int64_t a) -> int64_t {  // this subgroup's first item at or after unit start a
+    while (a < i1) {
+      const int64_t b = min(i1, (a / nb + 1) * (int64_t)nb);
+      if (a + sg < b) return a + sg;
+      a = b;
+    }
+    return -1;
+  };
   auto issue = [&](int64_t item) {
-    const int uu = (int)(item / A.nb);
-    const int bb = A.first_block + (int)(item % A.nb);
+    const int uu = (int)(item / nb);
+    const int bb = A.first_block + (int)(item % nb);
     const int row = (int)(c.blk_start[bb] - c.blk_start[A.first_block]);
     fence_proxy_async();
     mbar_arrive_expect_tx(xfull, 2 * 16384);
     tma_load_3d(X, tm, xfull, 0, row, uu);
     tma_load_3d(X + 16384, tm, xfull, 64, row, uu);
   };
-  if (gtid == 0 && i0 < i1) issue(i0);
-
-  int cur_u = -1;
+  if (w == 0 && lane == 0) {
+    const int64_t f = first_item(i0);
+    if (f >= 0) issue(f);
+  }
   uint32_t k = 0;
-  for (int64_t it = i0; it < i1; ++it, ++k) {
-    const int u = (int)(it / A.nb);
-    const int b = A.first_block + (int)(it % A.nb);
-    const int L = c.blk_len[b];
-    const int64_t start = c.blk_start[b];
-    const int64_t xrow0 = start - c.blk_start[A.first_block];  // source row of token 0
-    const __half* xsrc = src + (int64_t)u * A.unit_stride + xrow0 * 128;
+  for (int64_t a = i0; a < i1;) {
+    const int u = (int)(a / nb);
+    const int64_t bend = min(i1, (int64_t)(u + 1) * nb);
+    bar_side(SIDE);
+    stage_patterns(A, SIDE, u, sb, gtid);
+    bar_side(SIDE);
+    const int P = pt.flags()[0];
+    const float pmx = SIDE == 0 ? c.kpmax[u] : c.vpmax[u];
     const double* p64 = (SIDE == 0 ? c.kpat64 : c.vpat64) + (int64_t)u * c.Pcap * 128;
-    if (u != cur_u) {
-      bar_group(SIDE);
-      stage_patterns(A, SIDE, u, sb, gtid);
-      bar_group(SIDE);
-      cur_u = u;
-    }
-    const int P = pt.flags[0];
-    const uint32_t ph = k & 1;
-    const uint32_t tcol = tmem_base + SIDE * 64 + ph * 32;
-    mbar_wait(xfull, ph);
-    if (gtid == 0) {
-      tc_fence_after();
-      const uint32_t idesc = idesc_f16_f32(128, 32);
-      const uint64_t da0 = smem_desc_k_sw128(X), da1 = smem_desc_k_sw128(X + 16384);
-      const uint64_t dh0 = smem_desc_k_sw128(B), dh1 = smem_desc_k_sw128(B + 4096);
-      const uint64_t dl0 = smem_desc_k_sw128(B + 8192), dl1 = smem_desc_k_sw128(B + 12288);
+    for (int64_t it = a + sg; it < bend; it += 2, ++k) {
+      const int b = A.first_block + (int)(it % nb);
+      const int L = c.blk_len[b];
+      const int64_t start = c.blk_start[b];
+      const __half* xsrc = A.src[SIDE] + (int64_t)u * A.unit_stride + (start - c.blk_start[A.first_block]) * 128;
+      const int64_t blk = (int64_t)u * c.NBcap + b;
+      const uint32_t ph = k & 1;
+      const uint32_t tcol = tmem + sgi * 64 + ph * 32;
+      mbar_wait(xfull, ph);
+      if (w == 0 && lane == 0) {
+        tc_fence_after();
+        const uint32_t idesc = idesc_f16_f32(128, 32);
+        const uint64_t da0 = smem_desc_k_sw128(X), da1 = smem_desc_k_sw128(X + 16384);
+        const uint64_t dh0 = smem_desc_k_sw128(B), dh1 = smem_desc_k_sw128(B + 4096);
+        const uint64_t dl0 = smem_desc_k_sw128(B + 8192), dl1 = smem_desc_k_sw128(B + 12288);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over d = 128: D += x.hi, D += x.lo
-        const uint64_t o = 2 * (kk & 3);  // +32 B per K step inside the 128-B swizzle atom
-        mma_f16_ss(tcol, (kk < 4 ? da0 : da1) + o, (kk < 4 ? dh0 : dh1) + o, idesc, kk > 0 ? 1u : 0u);
-        mma_f16_ss(tcol, (kk < 4 ? da0 : da1) + o, (kk < 4 ? dl0 : dl1) + o, idesc, 1u);
-      }
-      mma_commit(mmab);
-    }
-
-    // ---- A. guess = argmin_p ||m'_p||^2 - 2 x.m'_p (thread per token, warps 0-3) ----------
-    const int tt_ = 32 * gw + lane;  // token of this thread in stages A/C
-    int guess = 0;
-    float Cg = 0.f, px = 0.f;
-    if (gw < 4) {
-      mbar_wait(mmab, ph);
-      tc_fence_after();
-      float best = FE_INF;
-#pragma unroll
-      for (int p0 = 0; p0 < 32; p0 += 16) {
-        uint32_t v[8], w[8];
-        tmem_ld8(tcol + p0 + ((uint32_t)(32 * gw) << 16), v);
-        tmem_ld8(tcol + p0 + 8 + ((uint32_t)(32 * gw) << 16), w);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          best = fminf(best, fkey(__fmaf_rn(-2.f, __uint_as_float(v[i]), pt.bb[p0 + i]), p0 + i, 0xffffffe0u));
-          best = fminf(best, fkey(__fmaf_rn(-2.f, __uint_as_float(w[i]), pt.bb[p0 + 8 + i]), p0 + 8 + i, 0xffffffe0u));
+        for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over d = 128: D += x.hi, D += x.lo
+          const uint64_t o = 2 * (kk & 3);  // +32 B per K step inside the 128-B swizzle atom
+          mma_f16_ss(tcol, (kk < 4 ? da0 : da1) + o, (kk < 4 ? dh0 : dh1) + o, idesc, kk > 0 ? 1u : 0u);
+          mma_f16_ss(tcol, (kk < 4 ? da0 : da1) + o, (kk < 4 ? dl0 : dl1) + o, idesc, 1u);
         }
+        mma_commit(mmab);
       }
-      guess = (int)(__float_as_uint(best) & 31u);
-      if (guess >= P) guess = 0;
-      Cg = best;
-      px = __fsub_rn(xt_at(X, tt_, pt.flags[2]), xt_at(X, tt_, pt.flags[3]));
-      tk.guess[tt_] = guess;
-      tc_fence_before();
-    }
-    bar_group(SIDE);
-
-    // ---- B. residual pass against the guess (all 8 warps, 16 tokens each) -------------
-    const int t0 = 16 * gw + g;
-    int idx[2] = {tk.guess[t0], tk.guess[t0 + 8]};
-    float r[2][8][4];
-    RowStats st;
-    resid_pass(X, M, gw, lane, idx, r, st);
-    float kmx[2], kmn[2], xmx[2], xmn[2];
+      token_stage(SIDE == 1, sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats);
+      const int64_t nxt = it + 2 < bend ? it + 2 : first_item(bend);
+      if constexpr (SIDE == 0) {
+        bar_sub(sgi);  // every token's final pattern index
+        if (st < L) c.kidx[blk * c.GP + st] = (int16_t)sc.fidx()[st];
+        uint32_t wreg[16];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      kmx[h] = qmax4(st.kmx[h]); kmn[h] = qmin4(st.kmn[h]);
-      xmx[h] = qmax4(st.xmx[h]); xmn[h] = qmin4(st.xmn[h]);
-      if (q == 0) {
-        tk.dg[t0 + 8 * h] = __fsub_rn(kmx[h], kmn[h]);
-        tk.ed[t0 + 8 * h] = derr(kmx[h], kmn[h], pt.mabsr[idx[h]]);
-        tk.xabs[t0 + 8 * h] = fmaxf(fabsf(xmx[h]), fabsf(xmn[h]));
-      }
-    }
-    bar_group(SIDE);
-
-    // ---- C. prune every other pattern by exact lower bounds (thread per token) ----------
-    if (gw < 4) {
-      tc_fence_after();
-      const float dg = tk.dg[tt_], xa = tk.xabs[tt_];
-      const float T2 = tk.ed[tt_];                  // >= |dg - d64(guess)|
-      const float dhi = __fadd_rn(dg, T2) * 1.0000002f;
-      const float dlo = fmaxf(__fsub_rn(dg, T2), 0.f) * 0.9999998f;
-      // Popoviciu: osc^2 >= 4 C / d; C_q >= C'_q - C'_g + C_g, C_g >= osc_g^2 / 2
-      const float theta = __fmaf_rn(32.f * dhi, dhi, -0.5f * dlo * dlo) * 1.000001f;
-      const float kap = TWO_M13 * 11.3137085f * xa;  // 2 x (tensor-core + split error) / ||m'||, ||x|| <= sqrt(d) |x|max
-      const float rhs = theta + Cg + kap * pt.mn[guess] + TWO_M17 * fabsf(Cg);
-      const bool nol2 = pt.flags[1] != 0;
-      const float pmx = SIDE == 0 ? c.kpmax[u] : c.vpmax[u];
-      const float pb = __fadd_rn(dhi, 4.76837158203125e-07f * (xa + pmx));  // probe: 2^-21 (|x| + |m|) rounding
-      uint32_t mask = 0;
+        for (int e = 0; e < 16; ++e) wreg[e] = 0u;
+        uint32_t badm[2];
+        int slow[2];
+#pragma unroll
+        for (int jc = 0; jc < 2; ++jc)
+          badm[jc] = L == 128 ? k_pass<BITS, true>(X, M, pt, sc, 2 * w + jc, lane, L, KW, wreg, &slow[jc])
+                              : k_pass<BITS, false>(X, M, pt, sc, 2 * w + jc, lane, L, KW, wreg, &slow[jc]);
+#pragma unroll
+        for (int jc = 0; jc < 2; ++jc)
+          if (slow[jc]) {
+            __syncwarp();
+            if (L == 128) k_slow<true>(X, M, pt, sc, 2 * w + jc, lane, L, p64, stats);
+            else k_slow<false>(X, M, pt, sc, 2 * w + jc, lane, L, p64, stats);
+          }
+        bar_sub(sgi);  // per-channel statistics of all 128 channels
+        k_scalar<BITS>(A, X, M, pt, sc, st, L, p64, blk, stats);
+        bar_sub(sgi);  // per-channel fp64 params in HBM
+#pragma unroll
+        for (int jc = 0; jc < 2; ++jc)
+          if (badm[jc]) k_fix<BITS>(c.kparam64, sc, 2 * w + jc, lane, badm[jc], xsrc, p64, blk, KW, wreg, stats);
+        if constexpr (BITS == 4) {  // word h + 2w of lane (tile tt) holds chunks 2w, 2w+1
+          uint32_t* dst = reinterpret_cast<uint32_t*>(c.kcodes + blk * c.blk_bytes);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) dst[((e >> 1) * 32 + lane) * 8 + (e & 1) + 2 * w] = wreg[e];
+        }
+      } else {
+        v_scalar<BITS>(A, X, M, pt, sc, st, L, start, u, blk, p64, stats);
+        __syncwarp();
 #pragma unroll 1
-      for (int p0 = 0; p0 < 32; p0 += 8) {
-        uint32_t v[8];
-        tmem_ld8(tcol + p0 + ((uint32_t)(32 * gw) << 16), v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int p = p0 + i;
-          const float bbp = pt.bb[p];
-          const float cp = __fmaf_rn(-2.f, __uint_as_float(v[i]), bbp);
-          const float lhs = __fmaf_rn(-TWO_M22, bbp, __fmaf_rn(-kap, pt.mn[p], __fmaf_rn(-TWO_M17, fabsf(cp), cp)));
-          const bool l2ok = nol2 || !(lhs > rhs);
-          const bool prok = fabsf(__fsub_rn(px, pt.pm[p])) <= pb;
-          mask |= (uint32_t)(l2ok && prok && p < P) << p;
-        }
+        for (int rs = 0; rs < 4; ++rs)
+          v_codes<BITS>(c.vcodes, c.vparam64, c.blk_bytes, c.Tcap, X, M, sc, 32 * w + 8 * rs, lane, L, u, start, blk, xsrc, p64, stats);
       }
-      tc_fence_before();
-      mask &= ~(1u << guess);
-      tk.cand[tt_] = mask;
-      if (stats && mask) atomicAdd(&stats[2], (unsigned)__popc(mask));
-    }
-    bar_group(SIDE);
-
-    // ---- D. survivors: full fp32 distance, top-2 with error bounds, fp64 re-match ---------
-    {
-      uint32_t cm[2] = {tk.cand[t0], tk.cand[t0 + 8]};
-      if (__any_sync(0xffffffffu, (cm[0] | cm[1]) != 0)) {
-        float best[2], bestE[2], low[2];
-        int bi[2] = {idx[0], idx[1]};
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          best[h] = __fsub_rn(kmx[h], kmn[h]);
-          bestE[h] = derr(kmx[h], kmn[h], pt.mabsr[idx[h]]);
-          low[h] = FE_INF;  // min over the other evaluated patterns of d - err
-        }
-        while (__any_sync(0xffffffffu, (cm[0] | cm[1]) != 0)) {
-          int pc[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            pc[h] = cm[h] ? __ffs(cm[h]) - 1 : -1;
-            cm[h] &= cm[h] - 1;
-          }
-          float s4[4];
-          cand_stats(X, M, gw, lane, pc[0] >= 0 ? pc[0] : idx[0], pc[1] >= 0 ? pc[1] : idx[1], s4);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float cx = qmax4(s4[2 * h]), cn = qmin4(s4[2 * h + 1]);
-            if (pc[h] >= 0) {
-              const float d = __fsub_rn(cx, cn), e = derr(cx, cn, pt.mabsr[pc[h]]);
-              if (d < best[h] || (d == best[h] && pc[h] < bi[h])) {
-                low[h] = fminf(low[h], best[h] - bestE[h]);
-                best[h] = d; bestE[h] = e; bi[h] = pc[h];
-              } else {
-                low[h] = fminf(low[h], d - e);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const bool amb = low[h] <= best[h] + bestE[h];
-          if (__any_sync(0xffffffffu, amb)) {
-            const int ri = refine64(X, t0 + 8 * h, p64, P, q);
-            if (amb) {
-              bi[h] = ri;
-              if (stats && q == 0) atomicAdd(&stats[0], 1u);
-            }
-          }
-        }
-        const bool chg = bi[0] != idx[0] || bi[1] != idx[1];
-        if (__any_sync(0xffffffffu, chg)) {
-          idx[0] = bi[0]; idx[1] = bi[1];
-          resid_pass(X, M, gw, lane, idx, r, st);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) { kmx[h] = qmax4(st.kmx[h]); kmn[h] = qmin4(st.kmn[h]); }
-        }
-      }
-      if (q == 0) { tk.fidx[t0] = idx[0]; tk.fidx[t0 + 8] = idx[1]; }
-    }
-    bar_group(SIDE);  // the x tile is free: prefetch the next item's span
-    if (gtid == 0 && it + 1 < i1) issue(it + 1);
-
-    if constexpr (SIDE == 0) {
-      // ================= K: per-channel groups over the span's tokens =================
-      float* R = reinterpret_cast<float*>(sb + OFF_R);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int t = t0 + 8 * h;
-        const bool ok = t < L;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          *reinterpret_cast<float2*>(R + t * RS + 16 * j + 2 * q) =
-              ok ? make_float2(r[h][j][0], r[h][j][1]) : make_float2(FE_NAN, FE_NAN);
-          *reinterpret_cast<float2*>(R + t * RS + 16 * j + 8 + 2 * q) =
-              ok ? make_float2(r[h][j][2], r[h][j][3]) : make_float2(FE_NAN, FE_NAN);
-        }
-      }
-      bar_group(SIDE);
-      const int c0 = 16 * gw + 2 * q;  // channels c0, c0+1, c0+8, c0+9 (k = 0..3)
-      float rr[8][2][4];
-      float lmx[4], lmn[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) { lmx[kk] = -FE_INF; lmn[kk] = FE_INF; }
-#pragma unroll
-      for (int tt = 0; tt < 8; ++tt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int t = 16 * tt + 8 * h + g;
-          const float2 a = *reinterpret_cast<const float2*>(R + t * RS + c0);
-          const float2 bq = *reinterpret_cast<const float2*>(R + t * RS + c0 + 8);
-          rr[tt][h][0] = a.x; rr[tt][h][1] = a.y; rr[tt][h][2] = bq.x; rr[tt][h][3] = bq.y;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const float key = fkey(rr[tt][h][kk], 2 * tt + h, 0xfffffff0u);
-            lmx[kk] = fmaxf(lmx[kk], key);
-            lmn[kk] = fminf(lmn[kk], key);
-          }
-        }
-      double* KQ = reinterpret_cast<double*>(sb + OFF_KQ);
-      float qlo[4], qinv[4], qhg[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int ch = c0 + (kk & 1) + 8 * (kk >> 1);
-        float gmx = lmx[kk], gmn = lmn[kk];
-#pragma unroll
-        for (int o = 4; o <= 16; o <<= 1) {
-          gmx = fmaxf(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
-          gmn = fminf(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
-        }
-        const float Rm = fmaxf(fabsf(gmx), fabsf(gmn));
-        const float Mc = pt.mabsc[ch];
-        // |key - r64| <= 2^-19 |r| + 2^-24 |r| + 2^-23 |m|: window of twice that
-        const float tolx = TWO_M17 * Rm + 4.76837158203125e-07f * Mc;
-        const float hib = gmx - tolx, lob = gmn + tolx;
-        int cnt = 0;
-#pragma unroll
-        for (int tt = 0; tt < 8; ++tt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float key = fkey(rr[tt][h][kk], 2 * tt + h, 0xfffffff0u);
-            cnt += (key >= hib) + (key <= lob);
-          }
-#pragma unroll
-        for (int o = 4; o <= 16; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        const uint32_t qm = 0x11111111u << q;
-        const uint32_t bmx = __ballot_sync(0xffffffffu, lmx[kk] == gmx) & qm;
-        const uint32_t bmn = __ballot_sync(0xffffffffu, lmn[kk] == gmn) & qm;
-        const bool fast = cnt == 2 && __popc(bmx) == 1 && __popc(bmn) == 1;
-        double hi64, lo64;
-        if (__all_sync(0xffffffffu, fast)) {
-          const int gx = (__ffs(bmx) - 1) >> 2, gn = (__ffs(bmn) - 1) >> 2;
-          const uint32_t ix = __float_as_uint(gmx) & 15u, in_ = __float_as_uint(gmn) & 15u;
-          const int tx = 16 * (int)(ix >> 1) + 8 * (int)(ix & 1) + gx;
-          const int tn = 16 * (int)(in_ >> 1) + 8 * (int)(in_ & 1) + gn;
-          hi64 = __dsub_rn((double)__half2float(xsrc[(int64_t)tx * 128 + ch]), p64[(int64_t)tk.fidx[tx] * 128 + ch]);
-          lo64 = __dsub_rn((double)__half2float(xsrc[(int64_t)tn * 128 + ch]), p64[(int64_t)tk.fidx[tn] * 128 + ch]);
-        } else {  // several elements inside the error window somewhere: fp64 over all of them
-          double dmx, dmn;
-          k_slow_extrema(R, tk.fidx, xsrc, p64, ch, g, hib, lob, &dmx, &dmn);
-#pragma unroll
-          for (int o = 4; o <= 16; o <<= 1) {
-            dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
-            dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
-          }
-          hi64 = dmx; lo64 = dmn;
-          if (stats && lane == q && !fast) atomicAdd(&stats[3], 1u);
-        }
-        const GroupQ gg = make_group(lo64, hi64, QMAX, A.yq, Rm, Mc);
-        qlo[kk] = gg.lo32; qinv[kk] = gg.inv; qhg[kk] = gg.hg;
-        if (g == 0) { KQ[ch] = gg.lo; KQ[128 + ch] = gg.scale; }
-      }
+      // release the x tile; the last warp out starts the next span's TMA into it
       __syncwarp();
-      // codes (pairs of channels c0+{0,1} / c0+{8,9} per token), K fragment words
-      uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW);
-      const int slot0 = 2 * (gw % HS);
-      const int wbase = 2 * (gw / HS);
-      const int swz = (lane / (32 / WL)) & (WL - 1);
-      uint32_t badm = 0;  // bit 2e + pr: element pair pr of (tt, h) = e lies in a guard band
-#pragma unroll
-      for (int tt = 0; tt < 8; ++tt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int t = 16 * tt + 8 * h + g;
-          bool bad0 = false, bad1 = false;
-          const float z0 = zcode(rr[tt][h][0], qlo[0], qinv[0], qhg[0], bad0);
-          const float z1 = zcode(rr[tt][h][1], qlo[1], qinv[1], qhg[1], bad0);
-          const float z2 = zcode(rr[tt][h][2], qlo[2], qinv[2], qhg[2], bad1);
-          const float z3 = zcode(rr[tt][h][3], qlo[3], qinv[3], qhg[3], bad1);
-          uint32_t p0 = zpair(z0, z1), p1 = zpair(z2, z3);
-          if (t >= L) { p0 = 0u; p1 = 0u; bad0 = bad1 = false; }
-          badm |= ((uint32_t)bad0 << (2 * (2 * tt + h))) | ((uint32_t)bad1 << (2 * (2 * tt + h) + 1));
-          const uint32_t part = (p0 << (slot0 * BITS)) | (p1 << ((slot0 + 1) * BITS));
-          atomicOr(&KW[(tt * 32 + lane) * WL + ((h + wbase) ^ swz)], part);
-        }
-      if (badm) {  // rare: the reference's fp64 sequence decides inside the guard band
-#pragma unroll 1
-        while (badm) {
-          const int bit = __ffs(badm) - 1;
-          badm &= badm - 1;
-          const int e = bit >> 1, pr = bit & 1, tt = e >> 1, h = e & 1;
-          const int t = 16 * tt + 8 * h + g, ch = c0 + 8 * pr;
-          const double* mrow = p64 + (int64_t)tk.fidx[t] * 128;
-          const __half* xrow = xsrc + (int64_t)t * 128;
-          const uint32_t pv = exact_code_at(xrow + ch, mrow + ch, KQ[ch], KQ[128 + ch], QMAX) |
-                              (exact_code_at(xrow + ch + 1, mrow + ch + 1, KQ[ch + 1], KQ[128 + ch + 1], QMAX) << 16);
-          const int sh = (slot0 + pr) * BITS;
-          uint32_t* wp = &KW[(tt * 32 + lane) * WL + ((h + wbase) ^ swz)];
-          atomicAnd(wp, ~(((uint32_t)QMAX | ((uint32_t)QMAX << 16)) << sh));
-          atomicOr(wp, pv << sh);
-          if (stats) atomicAdd(&stats[1], 1u);
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(rel, 1) == 3) {
+          *rel = 0;
+          if (nxt >= 0) issue(nxt);
         }
       }
-      // params
-      const int64_t blk = (int64_t)u * c.NBcap + b;
-      if (g == 0) {
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int ch = c0 + (kk & 1) + 8 * (kk >> 1);
-          c.kparam64[blk * 256 + ch] = KQ[128 + ch];
-          c.kparam64[blk * 256 + 128 + ch] = KQ[ch];
-          c.kparam32[blk * 2 * c.Dp + ch] = (float)KQ[128 + ch];
-          c.kparam32[blk * 2 * c.Dp + c.Dp + ch] = (float)KQ[ch];
-        }
-      }
-      if (gtid < L) c.kidx[blk * c.GP + gtid] = (int16_t)tk.fidx[gtid];
-      bar_group(SIDE);
-      // K words -> HBM (16 B per thread-chunk), clear for the next item
-      uint4* dst = reinterpret_cast<uint4*>(c.kcodes + blk * c.blk_bytes);
-      for (int ci = gtid; ci < 8 * 32 * WL / 4; ci += GT) {
-        uint32_t wv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int wi = 4 * ci + e, tl = wi / WL, w = wi % WL, ln = tl & 31;
-          const int a = tl * WL + (w ^ ((ln / (32 / WL)) & (WL - 1)));
-          wv[e] = KW[a];
-          KW[a] = 0u;
-        }
-        dst[ci] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-      }
-    } else {
-      // ================= V: per-token groups over channels =================
-      const int64_t blk = (int64_t)u * c.NBcap + b;
-      uint32_t words[WL];
-#pragma unroll
-      for (int w = 0; w < WL; ++w) words[w] = 0u;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int t = t0 + 8 * h;
-        const float xa = fmaxf(fabsf(xmx[h]), fabsf(xmn[h]));
-        const float Mr = pt.mabsr[idx[h]];
-        const float Rm = fmaxf(fabsf(kmx[h]), fabsf(kmn[h]));
-        // |key - r64| <= 2^-18 |r| + 2^-24 |r| + 2^-23 |m|: window of twice that
-        const float tolx = 1.52587890625e-05f * Rm + 4.76837158203125e-07f * Mr;
-        const float hib = kmx[h] - tolx, lob = kmn[h] + tolx;
-        int cnt = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
+      if constexpr (SIDE == 0 && BITS == 2) {
+        bar_sub(sgi);  // all code words of the block are in KW
+        uint4* dst = reinterpret_cast<uint4*>(c.kcodes + blk * c.blk_bytes);
+        constexpr int WL = 4;
+        for (int ci = st; ci < 8 * 32 * WL / 4; ci += 128) {
+          uint32_t wv[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float key = fkey(r[h][j][e], 4 * j + e, 0xffffffe0u);
-            cnt += (key >= hib) + (key <= lob);
+            const int wi = 4 * ci + e, tl = wi / WL, ww = wi % WL, ln = tl & 31;
+            const int ad = tl * WL + (ww ^ ((ln >> 3) & 3));
+            wv[e] = KW[ad];
+            KW[ad] = 0u;
           }
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-        const uint32_t gm = 0xfu << (4 * g);
-        const uint32_t bmx = __ballot_sync(0xffffffffu, st.kmx[h] == kmx[h]) & gm;
-        const uint32_t bmn = __ballot_sync(0xffffffffu, st.kmn[h] == kmn[h]) & gm;
-        const double* mrow = p64 + (int64_t)idx[h] * 128;
-        const __half* xrow = xsrc + (int64_t)t * 128;
-        double hi64, lo64;
-        const bool fast = cnt == 2 && __popc(bmx) == 1 && __popc(bmn) == 1;
-        if (__all_sync(0xffffffffu, fast)) {
-          const int qx = (__ffs(bmx) - 1) & 3, qn = (__ffs(bmn) - 1) & 3;
-          const uint32_t ix = __float_as_uint(kmx[h]) & 31u, in_ = __float_as_uint(kmn[h]) & 31u;
-          const int chx = 16 * (int)(ix >> 2) + 8 * (int)((ix >> 1) & 1) + 2 * qx + (int)(ix & 1);
-          const int chn = 16 * (int)(in_ >> 2) + 8 * (int)((in_ >> 1) & 1) + 2 * qn + (int)(in_ & 1);
-          hi64 = __dsub_rn((double)__half2float(xrow[chx]), mrow[chx]);
-          lo64 = __dsub_rn((double)__half2float(xrow[chn]), mrow[chn]);
-        } else {
-          double dmx, dmn;
-          v_slow_extrema(xrow, mrow, M + idx[h] * MR + q * 36, q, hib, lob, &dmx, &dmn);
-#pragma unroll
-          for (int o = 1; o <= 2; o <<= 1) {
-            dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
-            dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
-          }
-          hi64 = dmx; lo64 = dmn;
-          if (stats && q == 0 && t < L && !fast) atomicAdd(&stats[3], 1u);
-        }
-        // gate (gate.py:180-188; --no-v-gate flattens, engine.py:235-237)
-        const double raw = __dsub_rn((double)xmx[h], (double)xmn[h]);
-        const double flat = __dsub_rn(hi64, lo64);
-        const bool flatten = c.use_vgate ? (raw > 0.0 && gate_le(flat, raw, c.thr)) : true;
-        if (!flatten) {  // RAW payload: the exact input row (rare)
-          hi64 = (double)xmx[h]; lo64 = (double)xmn[h];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) r[h][j][e] = __half2float(xrow[16 * j + 8 * (e >> 1) + 2 * q + (e & 1)]);
-        }
-        const GroupQ gqv = flatten ? make_group(lo64, hi64, QMAX, A.yq, Rm, Mr) : make_group(lo64, hi64, QMAX, A.yq, xa, 0.f);
-        // codes -> pairs (token row, channel pair), exact fix-ups, movmatrix -> V^T fragment words
-        uint32_t pp[16];
-        uint32_t badm = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          bool bad0 = false, bad1 = false;
-          const float z0 = zcode(r[h][j][0], gqv.lo32, gqv.inv, gqv.hg, bad0);
-          const float z1 = zcode(r[h][j][1], gqv.lo32, gqv.inv, gqv.hg, bad0);
-          const float z2 = zcode(r[h][j][2], gqv.lo32, gqv.inv, gqv.hg, bad1);
-          const float z3 = zcode(r[h][j][3], gqv.lo32, gqv.inv, gqv.hg, bad1);
-          pp[2 * j] = zpair(z0, z1);
-          pp[2 * j + 1] = zpair(z2, z3);
-          badm |= ((uint32_t)bad0 << (2 * j)) | ((uint32_t)bad1 << (2 * j + 1));
-        }
-        if (t >= L) {
-          badm = 0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pp[i] = 0u;
-        }
-        if (badm) {  // rare: the reference's fp64 sequence decides inside the guard band
-          const double* mr = flatten ? mrow : nullptr;
-#pragma unroll 1
-          while (badm) {
-            const int i = __ffs(badm) - 1;
-            badm &= badm - 1;
-            const int ca = 16 * (i >> 1) + 8 * (i & 1) + 2 * q;
-            const uint32_t pv = exact_code_at(xrow + ca, mr ? mr + ca : nullptr, gqv.lo, gqv.scale, QMAX) |
-                                (exact_code_at(xrow + ca + 1, mr ? mr + ca + 1 : nullptr, gqv.lo, gqv.scale, QMAX) << 16);
-#pragma unroll
-            for (int k2 = 0; k2 < 16; ++k2) pp[k2] = k2 == i ? pv : pp[k2];
-            if (stats) atomicAdd(&stats[1], 1u);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t t0v = movm_t(pp[2 * j]), t1v = movm_t(pp[2 * j + 1]);  // hiRow 0 / 1 of sub-tile j
-          const int s0 = 2 * (j % HS);
-          words[h + 2 * (j / HS)] |= (t0v << (s0 * BITS)) | (t1v << ((s0 + 1) * BITS));
-        }
-        if (q == 0 && t < L) {
-          const int64_t tok = (int64_t)u * c.Tcap + start + t;
-          const int64_t slot = blk * c.GP + t;
-          c.vparam64[2 * tok] = gqv.scale;
-          c.vparam64[2 * tok + 1] = gqv.lo;
-          c.vparam32[2 * slot] = (float)gqv.scale;
-          c.vparam32[2 * slot + 1] = (float)gqv.lo;
-          c.vidx[slot] = (int16_t)(flatten ? idx[h] : RAW);
-          if (c.keep_diag && c.vdiag) { c.vdiag[2 * tok] = raw; c.vdiag[2 * tok + 1] = flat; }
+          dst[ci] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
-      uint4* dst = reinterpret_cast<uint4*>(c.vcodes + blk * c.blk_bytes + (size_t)(gw * 32 + lane) * WL * 4);
-#pragma unroll
-      for (int w = 0; w < WL; w += 4) dst[w / 4] = make_uint4(words[w], words[w + 1], words[w + 2], words[w + 3]);
     }
+    a = bend;
   }
 }
 
@@ -930,16 +1176,20 @@ encode_tc_kernel(const Args A, const __grid_constant__ CUtensorMap tmK, const __
   unsigned char* sb = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sb + OFF_BAR);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sb + OFF_BAR + 32);
-  uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW);
-  for (int i = tid; i < 8 * 32 * 8; i += NTHR) KW[i] = 0u;
+  int* rel = reinterpret_cast<int*>(sb + OFF_BAR + 64);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sb + OFF_BAR + 80);
+  if (BITS == 2) {
+    uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW);
+    for (int i = tid; i < 2 * SZ_KW / 4; i += NTHR) KW[i] = 0u;
+  }
+  if (tid < 4) rel[tid] = 0;
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
   }
-  if (warp == 0) tmem_alloc<128>(tslot);
+  if (warp == 0) tmem_alloc<256>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -947,12 +1197,12 @@ encode_tc_kernel(const Args A, const __grid_constant__ CUtensorMap tmK, const __
   const int64_t per = A.nitems / gridDim.x, rem = A.nitems % gridDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * per + min((int64_t)blockIdx.x, rem);
   const int64_t i1 = i0 + per + ((int64_t)blockIdx.x < rem ? 1 : 0);
-  if (warp < 8) run_side<BITS, 0>(A, sb, &tmK, tmem, i0, i1);
-  else run_side<BITS, 1>(A, sb, &tmV, tmem, i0, i1);
+  if (warp < 8) run_sub<BITS, 0>(A, sb, &tmK, tmem, i0, i1);
+  else run_sub<BITS, 1>(A, sb, &tmV, tmem, i0, i1);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_free<128>(tmem);
+  if (warp == 0) tmem_free<256>(tmem);
 }
 
 // TMA descriptor of a [U][rows][128] fp16 tensor (unit stride in elements), 64 x 128 x 1 boxes
@@ -1016,11 +1266,11 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
   }
   const int grid = (int)std::min<int64_t>(nsm, a.nitems);
   if (c.bits == 2) {
-    cudaFuncSetAttribute(fe::encode_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::SMEM_BYTES);
-    fe::encode_tc_kernel<2><<<grid, fe::NTHR, fe::SMEM_BYTES, st>>>(a, tk, tv);
+    cudaFuncSetAttribute(fe::encode_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::smem_bytes(2));
+    fe::encode_tc_kernel<2><<<grid, fe::NTHR, fe::smem_bytes(2), st>>>(a, tk, tv);
   } else {
-    cudaFuncSetAttribute(fe::encode_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::SMEM_BYTES);
-    fe::encode_tc_kernel<4><<<grid, fe::NTHR, fe::SMEM_BYTES, st>>>(a, tk, tv);
+    cudaFuncSetAttribute(fe::encode_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::smem_bytes(4));
+    fe::encode_tc_kernel<4><<<grid, fe::NTHR, fe::smem_bytes(4), st>>>(a, tk, tv);
   }
   return cudaGetLastError();
 }
