@@ -424,6 +424,13 @@ __device__ __forceinline__ float qmin4(float v) {
   v = fminf(v, __shfl_xor_sync(0xffffffffu, v, 1));
   return fminf(v, __shfl_xor_sync(0xffffffffu, v, 2));
 }
+// count of the two window tests as a negative number: set.*.s32 gives 0 / -1, one IADD3 per element
+__device__ __forceinline__ int win2(float key, float hib, float lob) {
+  int a, b;
+  asm("set.ge.s32.f32 %0, %1, %2;" : "=r"(a) : "f"(key), "f"(hib));
+  asm("set.le.s32.f32 %0, %1, %2;" : "=r"(b) : "f"(key), "f"(lob));
+  return a + b;
+}
 // bound on |d32 - d64| for a distance taken from keyed fp32 extrema (K1-TC):
 // key error 2^-18 |r|, fp32 residual error 2^-24 (|r| + 2|m|), subtraction 2^-24 |d|
 __device__ __forceinline__ float derr(float kmx, float kmn, float M) {
@@ -494,8 +501,7 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float key = fkey(r[h][j][e], 4 * j + e, 0xffffffe0u);
-          cnt += (key >= hib) + (key <= lob);
+          cnt -= win2(fkey(r[h][j][e], 4 * j + e, 0xffffffe0u), hib, lob);
         }
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
@@ -701,16 +707,20 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
   for (int e = 0; e < 16; ++e) fi[e] = sc.fidx()[16 * (e >> 1) + 8 * (e & 1) + g];
   float rr[16][4];
   k_load<FULL>(X, M, fi, jb, g, q, L, rr);
+  // keys replace r from here on: the codes below absorb their 2^-19 |r| error in the guard
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) rr[e][kk] = fkey(rr[e][kk], e, 0xfffffff0u);
   // all warp collectives first (no divergent code between them), then the per-channel results
   float lmx[4], lmn[4], gmx[4], gmn[4], hib[4], lob[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
     lmx[kk] = -FE_INF; lmn[kk] = FE_INF;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float key = fkey(rr[e][kk], e, 0xfffffff0u);
-      lmx[kk] = fmaxf(lmx[kk], key);
-      lmn[kk] = fminf(lmn[kk], key);
+    for (int e = 0; e < 16; e += 2) {
+      lmx[kk] = fmax3(lmx[kk], rr[e][kk], rr[e + 1][kk]);
+      lmn[kk] = fmin3(lmn[kk], rr[e][kk], rr[e + 1][kk]);
     }
     gmx[kk] = lmx[kk]; gmn[kk] = lmn[kk];
   }
@@ -732,17 +742,15 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
     hib[kk] = gmx[kk] - tolx; lob[kk] = gmn[kk] + tolx;
     cnt[kk] = 0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float key = fkey(rr[e][kk], e, 0xfffffff0u);
-      cnt[kk] += (key >= hib[kk]) + (key <= lob[kk]);
-    }
-    // fp32 params from the keyed extrema; |y - y_exact| <= inv (3 2^-19 R + 2^-21 (R + M) + 2^-23 span)
+    for (int e = 0; e < 16; ++e) cnt[kk] -= win2(rr[e][kk], hib[kk], lob[kk]);
+    // fp32 params from the keyed extrema, codes from the keys; |y - y_exact| <= inv (4 2^-19 R +
+    // 2^-21 (R + M) + 2^-23 span)
     // + qmax 2^-22 + 2^-24, doubled (K1-TC)
     const float span = __fsub_rn(gmx[kk], gmn[kk]);
     qlo[kk] = gmn[kk];
     if (span > 4.f * (3.814697265625e-06f * Rm + 4.76837158203125e-07f * (Rm + Mc))) {
       qinv[kk] = (float)QMAX * rcp_approx(span);
-      qhg[kk] = 0.5f - (qinv[kk] * (1.1444091796875e-05f * Rm + 9.5367431640625e-07f * (Rm + Mc) +
+      qhg[kk] = 0.5f - (qinv[kk] * (1.52587890625e-05f * Rm + 9.5367431640625e-07f * (Rm + Mc) +
                                     2.384185791015625e-07f * span) +
                         4.76837158203125e-07f * (float)QMAX + 1.1920928955078125e-07f);
     } else {  // (nearly) constant group: every code exact
