@@ -30,6 +30,11 @@ __device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2 (2^-22 rel), exp2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t lop3_magic(uint32_t w, uint32_t mask) {
   uint32_t r;
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(mask), "r"(0x64006400u));  // (w & mask) | magic
@@ -131,8 +136,8 @@ __device__ __forceinline__ void afrag(const uint32_t* w, int j, uint32_t* a) {
   for (int reg = 0; reg < 4; ++reg) {
     int word, slot;
     frag_word_slot(SIDE, 4 * j + reg, BITS, word, slot);
-    // K: raw 1024 + 2^k c (bias and 2^k folded into B); V: exact c (the PV
-    // accumulator runs over thousands of tiles and must not carry the bias)
+    // K: raw 1024 + 2^k c (bias and 2^k folded into B); V: exact c (the PV accumulator runs
+    // over thousands of tiles; a folded 1024 bias would cost it ~10 bits)
     a[reg] = SIDE == 0 ? slot_raw<BITS>(w[word], slot) : slot_exact<BITS>(w[word], slot);
   }
 }
@@ -197,74 +202,39 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
     return priv ? sW + (((size_t)warp * 8 + g) * max(Pv, 1) + p) * HN + 4 * nt + qd
                 : sW + ((size_t)warp * max(Pv, 1) + p) * MAXG + 4 * nt + qd;
   };
-  __half* myP = sP + warp * 256;
 
   const int b0 = chunk * a.bpc;
   const int b1 = min(a.nb, b0 + a.bpc);
-  // ---- cp.async pipeline over this warp's (block, tile) items -----------------------
-  // stage = K codes tile | V codes tile | kidx[16] | vidx[16] | vparam[16][2]
-  constexpr int KCB = WL * 4;                   // code bytes per lane per tile
-  constexpr int SB = (2 * 32 * KCB + 192 + 15) / 16 * 16;
-  unsigned char* ring = reinterpret_cast<unsigned char*>(sred + ATT_WARPS * MAXG * 4) + (size_t)warp * ATT_STAGES * SB;
+  // ---- register-prefetched tile stream: the lane's 16*BITS/8 code words per side come
+  // straight from HBM (fragment order makes them one contiguous vector per lane) while the
+  // previous tile computes; metadata: kidx / vidx / vparam of tokens g, g+8
+  constexpr int NW = 16 * BITS / 8;
   constexpr int tbytes = 16 * Dp * BITS / 8;
-  int pb = b0 + warp, pti = 0;                  // producer cursor
-  int pnt = 0;
-  // per-lane source pointers of the producer block: K/V code slices, and the
-  // 16-byte metadata slice this lane moves (lanes 0-1 kidx, 2-3 vidx, 4-11 vparam)
-  const uint8_t* ksrc = nullptr;
-  const uint8_t* vsrc = nullptr;
-  const uint8_t* msrc = nullptr;
-  const int minc = lane < 4 ? 32 : 128;         // metadata bytes per tile for this lane's array
-  auto set_block = [&]() {
-    if (pb >= b1) return;
-    const int64_t bo = (int64_t)u * c.NBcap + pb;
-    pnt = (c.blk_len[pb] + 15) >> 4;
-    ksrc = c.kcodes + bo * c.blk_bytes + lane * KCB;
-    vsrc = c.vcodes + bo * c.blk_bytes + lane * KCB;
-    const int64_t slot = bo * c.GP;
-    msrc = lane < 2 ? reinterpret_cast<const uint8_t*>(c.kidx + slot) + 16 * lane
-         : lane < 4 ? reinterpret_cast<const uint8_t*>(c.vidx + slot) + 16 * (lane - 2)
-                    : reinterpret_cast<const uint8_t*>(c.vparam32 + 2 * slot) + 16 * (lane - 4);
+  struct Tile {
+    uint32_t kw[NW], vw[NW];
+    int ki0, ki1, vi0, vi1;
+    float2 vp0, vp1;
   };
-  set_block();
-  auto issue = [&](int stage) {
-    unsigned char* st = ring + stage * SB;
-    if (pb < b1) {
-      if constexpr ((KCB & 15) == 0) {
-#pragma unroll
-        for (int o = 0; o < KCB; o += 16) {
-          cp_async16(st + lane * KCB + o, ksrc + o);
-          cp_async16(st + 32 * KCB + lane * KCB + o, vsrc + o);
-        }
-      } else {
-#pragma unroll
-        for (int o = 0; o < KCB; o += 4) {
-          cp_async4(st + lane * KCB + o, ksrc + o);
-          cp_async4(st + 32 * KCB + lane * KCB + o, vsrc + o);
-        }
-      }
-      if (lane < 12) cp_async16(st + 64 * KCB + 16 * lane, msrc);
-      ksrc += tbytes;
-      vsrc += tbytes;
-      msrc += minc;
-      if (++pti == pnt) {
-        pti = 0;
-        pb += ATT_WARPS;
-        set_block();
-      }
-    }
-    cp_async_commit();
+  auto load_tile = [&](int bb, int ti, Tile& t) {
+    const int64_t bo = (int64_t)u * c.NBcap + bb;
+    const uint8_t* kt = c.kcodes + bo * c.blk_bytes + (size_t)ti * tbytes;
+    const uint8_t* vt = c.vcodes + bo * c.blk_bytes + (size_t)ti * tbytes;
+    load_words<BITS>(kt, lane, t.kw, WL);
+    load_words<BITS>(vt, lane, t.vw, WL);
+    const int64_t slot = bo * c.GP + 16 * ti + g;
+    t.ki0 = __ldg(c.kidx + slot); t.ki1 = __ldg(c.kidx + slot + 8);
+    t.vi0 = __ldg(c.vidx + slot); t.vi1 = __ldg(c.vidx + slot + 8);
+    t.vp0 = __ldg(reinterpret_cast<const float2*>(c.vparam32) + slot);
+    t.vp1 = __ldg(reinterpret_cast<const float2*>(c.vparam32) + slot + 8);
   };
-#pragma unroll
-  for (int s = 0; s < ATT_STAGES - 1; ++s) issue(s);
+  // this lane's pattern-weight column base: W slot (p, head 4nt+qd) = wbase + p * wstride + 4nt
+  float* const wbase = priv ? sW + ((size_t)warp * 8 + g) * max(Pv, 1) * HN + qd : sW + (size_t)warp * max(Pv, 1) * MAXG + qd;
+  const int wstride = priv ? HN : MAXG;
 
   uint32_t bq[8][NT][2];
   float qz[NT], kbias[NT];
-  int L = 0;
-  int stage = 0;
-  for (int b = b0 + warp; b < b1; b += ATT_WARPS) {
-    L = c.blk_len[b];
-    const float* kp = c.kparam32 + ((int64_t)u * c.NBcap + b) * 2 * Dp;
+  auto block_setup = [&](int bb) {
+    const float* kp = c.kparam32 + ((int64_t)u * c.NBcap + bb) * 2 * Dp;
     // B fragments of 64 * 2^-k(c) * (q o s_b) (hi/lo columns), q.z_b per head, and
     // the per-column bias 1024 * sum_c B[c][col] the magic-number A operand adds
 #pragma unroll
@@ -301,63 +271,65 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       qz[nt] = __shfl_sync(0xffffffffu, zpart, 8 * qd);  // head 4nt+qd lives at g = 2qd
       kbias[nt] = 1024.f * (__shfl_sync(0xffffffffu, bpart, 8 * qd) + __shfl_sync(0xffffffffu, bpart, 8 * qd + 4));
     }
-    const int ntile = (L + 15) >> 4;
-    for (int ti = 0; ti < ntile; ++ti) {
-      cp_async_wait<ATT_STAGES - 2>();
-      __syncwarp();
-      const unsigned char* st = ring + stage * SB;
-      uint32_t kw[16 * BITS / 8], vw[16 * BITS / 8];
-      load_stage_words<BITS>(st + lane * KCB, kw, WL);
-      load_stage_words<BITS>(st + 32 * KCB + lane * KCB, vw, WL);
-      const int16_t* mk = reinterpret_cast<const int16_t*>(st + 64 * KCB);
-      const int16_t* mv = mk + 16;
-      const float2* mp = reinterpret_cast<const float2*>(st + 64 * KCB + 64);
-      const int r0 = 16 * ti + g, r1 = r0 + 8;
-      const bool ok0 = r0 < L, ok1 = r1 < L;
-      const int ki0 = mk[g], ki1 = mk[g + 8];
-      const int vi0 = ok0 ? mv[g] : -1, vi1 = ok1 ? mv[g + 8] : -1;
-      const float2 vp0 = ok0 ? mp[g] : make_float2(0.f, 0.f);
-      const float2 vp1 = ok1 ? mp[g + 8] : make_float2(0.f, 0.f);
-      __syncwarp();
-      issue((stage + ATT_STAGES - 1) % ATT_STAGES);  // refill the slot consumed last iteration
-      stage = (stage + 1) % ATT_STAGES;
+  };
 
-      // ---- S = K . (q o s): tokens on M, hi/lo head columns on N ----
-      // two accumulator chains (even / odd k-tiles) halve the dependent-MMA latency
-      float sacc[NT][4], sacc2[NT][4];
+  int b = b0 + warp, ti = 0;
+  Tile ta, tb;
+  if (b < b1) {
+    load_tile(b, 0, ta);
+    block_setup(b);
+  }
+  // one tile of block b (state cur), prefetching the next tile of the warp into nxt
+  auto step = [&](Tile& cur, Tile& nxt) {
+    const int L = c.blk_len[b];
+    const int ntile = (L + 15) >> 4;
+    int nb2 = b, nti = ti + 1;
+    if (nti >= ntile) { nb2 = b + ATT_WARPS; nti = 0; }
+    if (nb2 < b1) load_tile(nb2, nti, nxt);  // prefetch while this tile computes
+    const int r0 = 16 * ti + g, r1 = r0 + 8;
+    const bool ok0 = r0 < L, ok1 = r1 < L;
+    const int vi0 = ok0 ? cur.vi0 : -1, vi1 = ok1 ? cur.vi1 : -1;
+    const float2 vp0 = ok0 ? cur.vp0 : make_float2(0.f, 0.f);
+    const float2 vp1 = ok1 ? cur.vp1 : make_float2(0.f, 0.f);
+
+    // ---- S = K . (q o s): tokens on M, hi/lo head columns on N ----
+    // two accumulator chains (even / odd k-tiles) halve the dependent-MMA latency
+    float sacc[NT][4], sacc2[NT][4];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) { sacc[nt][r] = 0.f; sacc2[nt][r] = 0.f; }
+      for (int r = 0; r < 4; ++r) { sacc[nt][r] = 0.f; sacc2[nt][r] = 0.f; }
 #pragma unroll
-      for (int kt = 0; kt < 8; ++kt) {
-        if (kt < KT) {
-          uint32_t af[4];
-          afrag<BITS, 0>(kw, kt, af);
+    for (int kt = 0; kt < 8; ++kt) {
+      if (kt < KT) {
+        uint32_t af[4];
+        afrag<BITS, 0>(cur.kw, kt, af);
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma16816((kt & 1) ? sacc2[nt] : sacc[nt], af, bq[kt][nt][0], bq[kt][nt][1]);
-        }
+        for (int nt = 0; nt < NT; ++nt) mma16816((kt & 1) ? sacc2[nt] : sacc[nt], af, bq[kt][nt][0], bq[kt][nt][1]);
       }
+    }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) sacc[nt][r] += sacc2[nt][r];
-      // ---- online softmax (lazy rescale), P~ = p * s_t split hi/lo ----
-      uint32_t pt[NT][2];
+      for (int r = 0; r < 4; ++r) sacc[nt][r] += sacc2[nt][r];
+    // ---- online softmax (lazy rescale), P~ = p * s_t split hi/lo ----
+    uint32_t pt[NT][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int h = 4 * nt + qd;
-        const float add0 = qz[nt] + (ki0 >= 0 && ok0 ? sqm[ki0 * MAXG + h] : 0.f);
-        const float add1 = qz[nt] + (ki1 >= 0 && ok1 ? sqm[ki1 * MAXG + h] : 0.f);
-        const float s0 = ok0 ? fmaf(sacc[nt][0] + sacc[nt][1] - kbias[nt], 0.015625f, add0) * a.scale_log2 : -INFINITY;
-        const float s1 = ok1 ? fmaf(sacc[nt][2] + sacc[nt][3] - kbias[nt], 0.015625f, add1) * a.scale_log2 : -INFINITY;
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h = 4 * nt + qd;
+      const float add0 = qz[nt] + (cur.ki0 >= 0 && ok0 ? sqm[cur.ki0 * MAXG + h] : 0.f);
+      const float add1 = qz[nt] + (cur.ki1 >= 0 && ok1 ? sqm[cur.ki1 * MAXG + h] : 0.f);
+      const float s0 = ok0 ? fmaf(sacc[nt][0] + sacc[nt][1] - kbias[nt], 0.015625f, add0) * a.scale_log2 : -INFINITY;
+      const float s1 = ok1 ? fmaf(sacc[nt][2] + sacc[nt][3] - kbias[nt], 0.015625f, add1) * a.scale_log2 : -INFINITY;
+      // lazy rescale: only when some lane's score passes the running max by the threshold
+      if (__any_sync(0xffffffffu, fmaxf(s0, s1) > mrun[nt] + RESCALE_TH)) {
         float tmax = fmaxf(s0, s1);
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-        if (tmax > mrun[nt] + RESCALE_TH || mrun[nt] == -INFINITY) {
+        if (tmax > mrun[nt] + RESCALE_TH) {  // uniform over the 8 lanes of head 4nt+qd
           const float mnew = fmaxf(tmax, mrun[nt]);
-          const float alpha = mrun[nt] == -INFINITY ? 0.f : exp2f(mrun[nt] - mnew);
+          const float alpha = mrun[nt] == -INFINITY ? 0.f : fast_exp2(mrun[nt] - mnew);
           lsum[nt] *= alpha;
           zsum[nt] *= alpha;
 #pragma unroll
@@ -365,48 +337,55 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
 #pragma unroll
             for (int r = 0; r < 4; ++r) oacc[mt][nt][r] *= alpha;
           if (priv) {
-            for (int p = 0; p < Pv; ++p) *wslot(p, nt) *= alpha;
+            for (int p = 0; p < Pv; ++p) wbase[p * wstride + 4 * nt] *= alpha;
           } else {
-            for (int p = g; p < Pv; p += 8) *wslot(p, nt) *= alpha;
+            for (int p = g; p < Pv; p += 8) wbase[p * wstride + 4 * nt] *= alpha;
           }
           mrun[nt] = mnew;
         }
-        const float p0 = exp2f(s0 - mrun[nt]), p1 = exp2f(s1 - mrun[nt]);
-        lsum[nt] += p0 + p1;
-        zsum[nt] = fmaf(p0, vp0.y, fmaf(p1, vp1.y, zsum[nt]));
-        if (priv) {
-          if (vi0 >= 0) *wslot(vi0, nt) += p0;
-          if (vi1 >= 0) *wslot(vi1, nt) += p1;
-        } else {
-          __syncwarp();  // rescaled W visible before other lanes add into it
-          if (vi0 >= 0 && p0 != 0.f) atomicAdd(wslot(vi0, nt), p0);
-          if (vi1 >= 0 && p1 != 0.f) atomicAdd(wslot(vi1, nt), p1);
-        }
-        const float w0 = p0 * vp0.x, w1 = p1 * vp1.x;
-        const __half2 wh = __floats2half2_rn(w0, w1);
-        const float2 wb = __half22float2(wh);
-        const __half2 wl = __floats2half2_rn(w0 - wb.x, w1 - wb.y);
-        // P~ rows g / g+8 (cols 2qd, 2qd+1 = hi, lo of head 4nt+qd) are C-fragment
-        // 8x8 b16 tiles; their transposes are exactly the PV B fragments (k = token, n = col)
-        const __half2 r0 = __halves2half2(__low2half(wh), __low2half(wl));
-        const __half2 r1 = __halves2half2(__high2half(wh), __high2half(wl));
-        pt[nt][0] = movmatrix_t(*reinterpret_cast<const uint32_t*>(&r0));
-        pt[nt][1] = movmatrix_t(*reinterpret_cast<const uint32_t*>(&r1));
       }
-      // ---- O^T += V^T . P~ : channels on M ----
-      uint32_t (&bp)[NT][2] = pt;
+      const float p0 = fast_exp2(s0 - mrun[nt]), p1 = fast_exp2(s1 - mrun[nt]);
+      lsum[nt] += p0 + p1;
+      zsum[nt] = fmaf(p0, vp0.y, fmaf(p1, vp1.y, zsum[nt]));
+      if (priv) {
+        if (vi0 >= 0) wbase[vi0 * wstride + 4 * nt] += p0;
+        if (vi1 >= 0) wbase[vi1 * wstride + 4 * nt] += p1;
+      } else {
+        __syncwarp();  // rescaled W visible before other lanes add into it
+        if (vi0 >= 0 && p0 != 0.f) atomicAdd(&wbase[vi0 * wstride + 4 * nt], p0);
+        if (vi1 >= 0 && p1 != 0.f) atomicAdd(&wbase[vi1 * wstride + 4 * nt], p1);
+      }
+      const float w0 = p0 * vp0.x, w1 = p1 * vp1.x;
+      const __half2 wh = __floats2half2_rn(w0, w1);
+      const float2 wb = __half22float2(wh);
+      const __half2 wl = __floats2half2_rn(w0 - wb.x, w1 - wb.y);
+      // P~ rows g / g+8 (cols 2qd, 2qd+1 = hi, lo of head 4nt+qd) are C-fragment
+      // 8x8 b16 tiles; their transposes are exactly the PV B fragments (k = token, n = col)
+      const __half2 rr0 = __halves2half2(__low2half(wh), __low2half(wl));
+      const __half2 rr1 = __halves2half2(__high2half(wh), __high2half(wl));
+      pt[nt][0] = movmatrix_t(*reinterpret_cast<const uint32_t*>(&rr0));
+      pt[nt][1] = movmatrix_t(*reinterpret_cast<const uint32_t*>(&rr1));
+    }
+    // ---- O^T += V^T . P~ : channels on M ----
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        if (mt < KT) {
-          uint32_t af[4];
-          afrag<BITS, 1>(vw, mt, af);
+    for (int mt = 0; mt < 8; ++mt) {
+      if (mt < KT) {
+        uint32_t af[4];
+        afrag<BITS, 1>(cur.vw, mt, af);
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma16816(oacc[mt][nt], af, bp[nt][0], bp[nt][1]);
-        }
+        for (int nt = 0; nt < NT; ++nt) mma16816(oacc[mt][nt], af, pt[nt][0], pt[nt][1]);
       }
     }
+    ti = nti;
+    if (nb2 != b) {
+      b = nb2;
+      if (b < b1) block_setup(b);
+    }
+  };
+  while (b < b1) {
+    step(ta, tb);
+    ta = tb;
   }
-  cp_async_wait<0>();
 
   // ---- merge the warps of the CTA --------------------------------------------------
   // per-head running max m (same for the 8 lanes of a head), l and z partial per lane
@@ -544,11 +523,10 @@ __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_s
 }
 
 size_t attn_smem_bytes(int Dp, int Pk, int Pv, int bits, int NT) {
-  const int SB = round_up(2 * 32 * frag_words_per_lane(Dp, bits) * 4 + 192, 16);
   const size_t wfl = attn_w_private(Pv, NT) ? (size_t)ATT_WARPS * 8 * max(Pv, 1) * 4 * NT
                                              : (size_t)ATT_WARPS * max(Pv, 1) * MAXG;
   return (size_t)MAXG * Dp * 4 + (size_t)max(Pk, 1) * MAXG * 4 + wfl * 4 + (size_t)max(Pv, 1) * MAXG * 4 +
-         ATT_WARPS * 256 * 2 + ATT_WARPS * MAXG * 4 * 4 + (size_t)ATT_WARPS * ATT_STAGES * SB + 16;
+         ATT_WARPS * 256 * 2 + ATT_WARPS * MAXG * 4 * 4 + 16;
 }
 
 template <int BITS, int NT, int KT>
