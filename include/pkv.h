@@ -132,6 +132,22 @@ int pkv_dequant(pkv_cache* c, int64_t t0, int64_t t1, double* k_out, double* v_o
  * (token-major) for K and V; pack with pkv_pack_codes for the reference bytes. */
 int pkv_export_codes(pkv_cache* c, int64_t t0, int64_t t1, uint8_t* k_codes, uint8_t* v_codes, void* stream);
 
+/* Resume: install a committed state (reference snapshot.py:148-220 load_snapshot ->
+ * engine HeadCacheState) into the cache, replacing its contents.  All units share the
+ * token count and block geometry (lockstep).  Host: blk_start/blk_len [nb] (the
+ * first nb_prefill blocks are prefill spans, the rest decode flushes of G), nk/nv
+ * [U] pattern counts, npk/npv [U] how many of them came from prefill mining.
+ * Device: kpat/vpat fp64 [U][Pk|Pv][D]; kparam fp64 [U][nb][2][D] (scale, zero);
+ * kidx/vidx int32 [U][C] (RAW = -1); vparam fp64 [U][C][2]; kcodes/vcodes uint8
+ * [U][C][D] unpacked; wk/wv [U][win][D] in the cache dtype; kdiag/vdiag fp64
+ * [U][C][2] (raw, flat) or NULL.  C = sum(blk_len). */
+int pkv_cache_import(pkv_cache* c, int64_t token_count, int32_t nb, const int64_t* blk_start, const int32_t* blk_len,
+                     int32_t nb_prefill, int32_t win_len, int32_t Pk, int32_t Pv, const int32_t* nk,
+                     const int32_t* nv, const double* kpat, const double* vpat, const double* kparam,
+                     const int32_t* kidx, const int32_t* vidx, const double* vparam, const uint8_t* kcodes,
+                     const uint8_t* vcodes, const void* wk, const void* wv, const double* kdiag,
+                     const double* vdiag, void* stream);
+
 /* Raw device arena pointers of the cache (read-only views for export / PKVS
  * snapshots): name in {"kpat64","vpat64","kparam64","vparam64","kidx","vidx",
  * "kdiag","vdiag","wk","wv","nk","nv","blk_start","blk_len","kcodes","vcodes"}. */

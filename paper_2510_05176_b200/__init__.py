@@ -43,6 +43,15 @@ from .patterns import (
     reconstruct_vector,
 )
 from .quant import QuantizedGroup, QuantParams, dequantize_group, pack_codes, quantize_group, unpack_codes
+from .snapshot import (
+    SNAPSHOT_MAGIC,
+    SNAPSHOT_VERSION,
+    cache_snapshot_bytes,
+    load_snapshot,
+    restore_cache,
+    save_cache_snapshot,
+    save_snapshot,
+)
 
 __version__ = "0.1.0"
 
@@ -54,5 +63,6 @@ __all__ = [
     "GateDecision", "contraction_threshold", "decide", "expected_error_gain", "z_quantile", "PatternMatch",
     "PatternSet", "lloyd_kmeans", "match_many", "match_pattern", "midrange_center", "mine_patterns",
     "minmax_distance", "reconstruct_vector", "QuantizedGroup", "QuantParams", "dequantize_group", "pack_codes",
-    "quantize_group", "unpack_codes",
+    "quantize_group", "unpack_codes", "SNAPSHOT_MAGIC", "SNAPSHOT_VERSION", "save_snapshot", "load_snapshot",
+    "save_cache_snapshot", "cache_snapshot_bytes", "restore_cache",
 ]

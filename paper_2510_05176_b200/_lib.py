@@ -71,6 +71,8 @@ PROTOTYPES = {
     "pkv_decode_attn": (C.c_int, [_vp, _vp, _i32, _f32, _vp, _vp]),
     "pkv_dequant": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "pkv_export_codes": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "pkv_cache_import": (C.c_int, [_vp, _i64, _i32, _P(_i64), _P(_i32), _i32, _i32, _i32, _i32, _P(_i32), _P(_i32),
+                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pkv_cache_buffer": (C.c_int, [_vp, C.c_char_p, _P(_vp), _P(_i64)]),
     "pkv_cache_read": (C.c_int, [_vp, C.c_char_p, _i64, _i64, _vp, _vp]),
     "pkv_quantize_groups": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),

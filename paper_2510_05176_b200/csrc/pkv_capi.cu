@@ -491,6 +491,100 @@ extern "C" int pkv_mine(pkv_cache* c, int32_t side, const void* x, int64_t T, co
   return mine_impl(c, 1 << side, x, x, T, first_idx, first_idx, history, niter, (cudaStream_t)stream);
 }
 
+// pattern tables with per-unit counts (device [U][P][D] fp64, host counts [U] <= P)
+static int load_patterns(pkv_cache* c, int side, const double* pat, int P, const int32_t* counts, cudaStream_t st) {
+  DevCache& d = c->dev;
+  double* p64 = side == 0 ? d.kpat64 : d.vpat64;
+  float* p32 = side == 0 ? d.kpat32 : d.vpat32;
+  std::vector<double> h((size_t)c->U * P * c->D);
+  if (P > 0) CU(cudaMemcpyAsync(h.data(), pat, h.size() * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::vector<double> h64((size_t)c->U * d.Pcap * c->D, 0.0);
+  std::vector<float> h32((size_t)c->U * d.Pcap * d.Dp, 0.f);
+  std::vector<float> pm(c->U, 0.f);
+  std::vector<int> n(c->U, 0);
+  int bound = 0;
+  for (int u = 0; u < c->U; ++u) {
+    n[u] = counts ? counts[u] : P;
+    bound = std::max(bound, n[u]);
+    for (int p = 0; p < n[u]; ++p)
+      for (int ch = 0; ch < c->D; ++ch) {
+        const double v = h[((size_t)u * P + p) * c->D + ch];
+        h64[((size_t)u * d.Pcap + p) * c->D + ch] = v;
+        h32[((size_t)u * d.Pcap + p) * d.Dp + ch] = (float)v;
+        pm[u] = std::max(pm[u], (float)std::fabs(v) * (1.f + 1e-6f));
+      }
+  }
+  CU(cudaMemcpyAsync(p64, h64.data(), h64.size() * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(p32, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(side == 0 ? d.kpmax : d.vpmax, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(side == 0 ? d.nk : d.nv, n.data(), n.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(launch_probes(d, st));
+  CU(cudaStreamSynchronize(st));
+  if (side == 0) c->pk_bound = bound; else c->pv_bound = bound;
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_import(pkv_cache* c, int64_t token_count, int32_t nb, const int64_t* blk_start,
+                                const int32_t* blk_len, int32_t nb_prefill, int32_t win_len, int32_t Pk, int32_t Pv,
+                                const int32_t* nk, const int32_t* nv, const double* kpat, const double* vpat,
+                                const double* kparam, const int32_t* kidx, const int32_t* vidx, const double* vparam,
+                                const uint8_t* kcodes, const uint8_t* vcodes, const void* wk, const void* wv,
+                                const double* kdiag, const double* vdiag, void* stream) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  const pkv_config& cfg = c->cfg;
+  const int G = cfg.group_size, W = cfg.residual_window;
+  if (nb < 0 || nb_prefill < 0 || nb_prefill > nb || win_len < 0 || Pk < 0 || Pv < 0 || token_count < 0)
+    return fail(PKV_USAGE, -1, "invalid import geometry");
+  if (nb > 0 && (!blk_start || !blk_len || !kparam || !kidx || !vidx || !vparam || !kcodes || !vcodes))
+    return fail(PKV_USAGE, -1, "null argument");
+  int64_t C = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (blk_len[b] < 1 || blk_len[b] > G || blk_start[b] != C)
+      return fail(PKV_DATA, b, "block %d: start %lld / length %d do not continue the committed tokens", b,
+                  (long long)blk_start[b], blk_len[b]);
+    if (b >= nb_prefill && blk_len[b] != G) return fail(PKV_DATA, b, "decode block %d has length %d != G", b, blk_len[b]);
+    C += blk_len[b];
+  }
+  if (C + win_len != token_count)
+    return fail(PKV_DATA, -1, "committed %lld + window %d != token count %lld", (long long)C, win_len,
+                (long long)token_count);
+  if (win_len > W + G - 1) return fail(PKV_DATA, -1, "window of %d rows exceeds W + G - 1 = %d", win_len, W + G - 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = pkv_cache_reset(c, 0, stream);
+  if (rc) return rc;
+  rc = reserve(c, std::max<int64_t>(c->dev.Tcap, token_count + 4 * G), std::max(c->dev.Pcap, std::max(Pk, Pv) + 8), st);
+  if (rc) return rc;
+  while ((int64_t)nb + 2 > c->dev.NBcap) {
+    rc = reserve(c, c->dev.Tcap * 2, c->dev.Pcap, st);
+    if (rc) return rc;
+  }
+  if (Pk > 0 && cfg.use_k_patterns) { rc = load_patterns(c, 0, kpat, Pk, nk, st); if (rc) return rc; }
+  if (Pv > 0 && cfg.use_v_patterns) { rc = load_patterns(c, 1, vpat, Pv, nv, st); if (rc) return rc; }
+  DevCache& d = c->dev;
+  c->blk_start.assign(blk_start, blk_start + nb);
+  c->blk_len.assign(blk_len, blk_len + nb);
+  c->nb = nb;
+  c->nb_prefill = nb_prefill;
+  c->decode_base = nb_prefill > 0 ? blk_start[nb_prefill - 1] + blk_len[nb_prefill - 1] : 0;
+  rc = upload_blocks(c, st);
+  if (rc) return rc;
+  CU(launch_import(d, nb, C, kparam, kidx, vidx, vparam, kcodes, vcodes, kdiag, vdiag, st));
+  if (win_len > 0) {
+    const size_t row = (size_t)c->D * c->esize;
+    CU(cudaMemcpy2DAsync(d.wk, (size_t)d.Wcap * row, wk, (size_t)win_len * row, (size_t)win_len * row, c->U,
+                         cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpy2DAsync(d.wv, (size_t)d.Wcap * row, wv, (size_t)win_len * row, (size_t)win_len * row, c->U,
+                         cudaMemcpyDeviceToDevice, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  c->win_slot0 = 0;
+  c->win_len = win_len;
+  c->token_count = token_count;
+  c->committed = C;
+  return PKV_OK;
+}
+
 extern "C" int pkv_set_patterns(pkv_cache* c, int32_t side, const double* pat, int32_t P, void* stream) {
   if (!c) return fail(PKV_USAGE, -1, "null cache");
   if (P < 0) return fail(PKV_USAGE, -1, "negative pattern count");

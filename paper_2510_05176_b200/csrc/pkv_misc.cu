@@ -218,6 +218,97 @@ cudaError_t launch_codes(const DevCache& c, int nb, int64_t t0, int64_t n, uint8
   return cudaGetLastError();
 }
 
+// ---- state import (resume from a PKVS snapshot, reference snapshot.py:148-220) ---------------
+// Per committed token t of unit u (reference layout in, arena layout out): indices and V
+// params into their block slots, fp64 params by token, gate records.
+__global__ void import_tokens_kernel(DevCache c, int nb, int64_t C, const int32_t* kidx, const int32_t* vidx,
+                                     const double* vparam, const double* kdiag, const double* vdiag) {
+  const int u = blockIdx.y;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < C; t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = find_block(c.blk_start, nb, t);
+    const int64_t slot = ((int64_t)u * c.NBcap + b) * c.GP + (t - c.blk_start[b]);
+    const int64_t i = (int64_t)u * C + t;
+    c.kidx[slot] = (int16_t)kidx[i];
+    c.vidx[slot] = (int16_t)vidx[i];
+    const int64_t tok = (int64_t)u * c.Tcap + t;
+    c.vparam64[2 * tok] = vparam[2 * i];
+    c.vparam64[2 * tok + 1] = vparam[2 * i + 1];
+    c.vparam32[2 * slot] = (float)vparam[2 * i];
+    c.vparam32[2 * slot + 1] = (float)vparam[2 * i + 1];
+    if (c.keep_diag) {
+      if (kdiag && c.kdiag) { c.kdiag[2 * tok] = kdiag[2 * i]; c.kdiag[2 * tok + 1] = kdiag[2 * i + 1]; }
+      if (vdiag && c.vdiag) { c.vdiag[2 * tok] = vdiag[2 * i]; c.vdiag[2 * tok + 1] = vdiag[2 * i + 1]; }
+    }
+  }
+}
+// Per block: K params (fp64 and the fp32 attention copy, padded to Dp)
+__global__ void import_kparams_kernel(DevCache c, int nb, const double* kparam) {
+  const int u = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nb * c.Dp;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / c.Dp), ch = (int)(i % c.Dp);
+    const int64_t blk = (int64_t)u * c.NBcap + b;
+    double sc = 0.0, z = 0.0;
+    if (ch < c.D) {
+      sc = kparam[(((int64_t)u * nb + b) * 2) * c.D + ch];
+      z = kparam[(((int64_t)u * nb + b) * 2 + 1) * c.D + ch];
+      c.kparam64[blk * 2 * c.D + ch] = sc;
+      c.kparam64[blk * 2 * c.D + c.D + ch] = z;
+    }
+    c.kparam32[blk * 2 * c.Dp + ch] = (float)sc;
+    c.kparam32[blk * 2 * c.Dp + c.Dp + ch] = (float)z;
+  }
+}
+// Per (block, tile, lane, word): the mma-fragment code words from unpacked codes [U][C][D]
+// (the same word assembly as stage E of encode_span_kernel)
+__global__ void import_codes_kernel(DevCache c, int nb, int64_t C, const uint8_t* kcodes, const uint8_t* vcodes) {
+  const int u = blockIdx.y;
+  const int WL = frag_words_per_lane(c.Dp, c.bits), S = 16 / c.bits;
+  const int64_t nw = (int64_t)nb * c.ntile_blk * 32 * WL;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * nw; i += (int64_t)gridDim.x * blockDim.x) {
+    const int side = i >= nw;
+    const int64_t k = side ? i - nw : i;
+    const int wl = (int)(k % WL), ln = (int)((k / WL) % 32);
+    const int tile = (int)((k / (WL * 32)) % c.ntile_blk), b = (int)(k / ((int64_t)WL * 32 * c.ntile_blk));
+    const int g = ln >> 2, q = ln & 3;
+    const int64_t s0 = c.blk_start[b];
+    const int L = c.blk_len[b];
+    const uint8_t* src = (side ? vcodes : kcodes) + (int64_t)u * C * c.D;
+    auto code = [&](int t, int ch) -> uint32_t {
+      return (t < L && ch < c.D && s0 + t < C) ? src[(s0 + t) * c.D + ch] : 0u;
+    };
+    uint32_t word = 0;
+    for (int s2 = 0; s2 < S; ++s2) {
+      const int R = frag_reg_of(side, wl, s2, c.bits);
+      const int j = R >> 2, reg = R & 3;
+      const int row = g + 8 * (reg & 1), col = 2 * q + 8 * (reg >> 1);
+      const int shift = s2 * c.bits;
+      if (side == 0) {
+        const int t = tile * 16 + row, c0 = 16 * j + col;
+        word |= code(t, c0) << shift;
+        word |= code(t, c0 + 1) << (16 + shift);
+      } else {
+        const int ch = 16 * j + row, t0 = tile * 16 + col;
+        word |= code(t0, ch) << shift;
+        word |= code(t0 + 1, ch) << (16 + shift);
+      }
+    }
+    uint8_t* dst = (side ? c.vcodes : c.kcodes) + ((int64_t)u * c.NBcap + b) * c.blk_bytes;
+    reinterpret_cast<uint32_t*>(dst)[((int64_t)tile * 32 + ln) * WL + wl] = word;
+  }
+}
+cudaError_t launch_import(const DevCache& c, int nb, int64_t C, const double* kparam, const int32_t* kidx,
+                          const int32_t* vidx, const double* vparam, const uint8_t* kcodes, const uint8_t* vcodes,
+                          const double* kdiag, const double* vdiag, cudaStream_t st) {
+  if (nb <= 0 || C <= 0) return cudaSuccess;
+  const int gx = (int)imin64((C + 255) / 256, 1024);
+  import_tokens_kernel<<<dim3(gx, c.U), 256, 0, st>>>(c, nb, C, kidx, vidx, vparam, kdiag, vdiag);
+  import_kparams_kernel<<<dim3((int)imin64(((int64_t)nb * c.Dp + 255) / 256, 1024), c.U), 256, 0, st>>>(c, nb, kparam);
+  const int64_t nw = 2 * (int64_t)nb * c.ntile_blk * 32 * frag_words_per_lane(c.Dp, c.bits);
+  import_codes_kernel<<<dim3((int)imin64((nw + 255) / 256, 4096), c.U), 256, 0, st>>>(c, nb, C, kcodes, vcodes);
+  return cudaGetLastError();
+}
+
 // ---- group API ------------------------------------------------------------------------
 // quantize_group over many groups: values fp64 concatenated, offsets[n+1].
 // One warp per group (quant.py:70-111).

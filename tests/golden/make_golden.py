@@ -245,6 +245,42 @@ def gen_acceptance():
         json.dump(doc, f, indent=1)
 
 
+SNAPSHOT_CASES = {
+    # name: (EngineConfig kwargs, head_dim, prefill, decode, [(layer, head, seed), ...])
+    "k_gate": (dict(bits=2, pattern_count=8, use_k_gate=True), 64, 400, 140, [(0, 0, 21), (0, 1, 22), (1, 0, 23)]),
+    "no_vgate4": (dict(bits=4, pattern_count=8, use_v_gate=False), 32, 300, 150, [(0, 0, 31), (2, 3, 32)]),
+    "short": (dict(bits=2, pattern_count=4), 16, 100, 60, [(0, 0, 41), (0, 1, 42), (0, 2, 43), (5, 7, 44)]),
+    "raw8": (dict(bits=8, pattern_count=4, group_size=32, residual_window=32, use_k_patterns=False,
+                  use_v_patterns=False, generate_new_patterns=False), 32, 100, 40, [(0, 0, 51), (0, 1, 52)]),
+}
+
+
+def gen_snapshot():
+    """Reference PKVS images (snapshot.py:57-99) of multi-head replays; the inputs are the
+    synthetic generator's, cast to fp16 (so the GPU replays exactly the same values)."""
+    import tempfile
+    from patternkv import snapshot
+
+    out = {}
+    for name, (kw, d, tp, td, heads) in SNAPSHOT_CASES.items():
+        cfg = engine.EngineConfig(**kw)
+        states = {}
+        for layer, head, seed in heads:
+            s = analysis.generate_synthetic_stream(synth_spec(seed, tp + td, d))
+            k = s.prefill_k[0, 0].astype(np.float16).astype(np.float64)
+            v = s.prefill_v[0, 0].astype(np.float16).astype(np.float64)
+            states[(layer, head)] = engine.replay_head(k[:tp], v[:tp], k[tp:], v[tp:], cfg)
+        with tempfile.NamedTemporaryFile(suffix=".pkvs") as f:
+            snapshot.save_snapshot(f.name, states)
+            blob = open(f.name, "rb").read()
+        p = name + "__"
+        out[p + "config"] = np.array(json.dumps(kw))
+        out[p + "dims"] = np.array([d, tp, td], np.int64)
+        out[p + "heads"] = np.array(heads, np.int64)
+        out[p + "blob"] = np.frombuffer(blob, np.uint8)
+    save("snapshot.npz", **out)
+
+
 if __name__ == "__main__":
     gen_quant()
     gen_match()
@@ -253,4 +289,5 @@ if __name__ == "__main__":
     gen_synth()
     gen_engine()
     gen_acceptance()
+    gen_snapshot()
     print("golden fixtures written to", HERE)
