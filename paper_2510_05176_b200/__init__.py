@@ -43,6 +43,7 @@ from .patterns import (
     reconstruct_vector,
 )
 from .quant import QuantizedGroup, QuantParams, dequantize_group, pack_codes, quantize_group, unpack_codes
+from .trace import TraceHeader, ingest_trace, load_trace_device, read_trace, read_trace_header, write_trace
 from .snapshot import (
     SNAPSHOT_MAGIC,
     SNAPSHOT_VERSION,
@@ -64,5 +65,6 @@ __all__ = [
     "PatternSet", "lloyd_kmeans", "match_many", "match_pattern", "midrange_center", "mine_patterns",
     "minmax_distance", "reconstruct_vector", "QuantizedGroup", "QuantParams", "dequantize_group", "pack_codes",
     "quantize_group", "unpack_codes", "SNAPSHOT_MAGIC", "SNAPSHOT_VERSION", "save_snapshot", "load_snapshot",
-    "save_cache_snapshot", "cache_snapshot_bytes", "restore_cache",
+    "save_cache_snapshot", "cache_snapshot_bytes", "restore_cache", "TraceHeader", "write_trace", "read_trace",
+    "read_trace_header", "load_trace_device", "ingest_trace",
 ]

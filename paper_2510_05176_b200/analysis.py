@@ -1,6 +1,6 @@
 """Storage accounting closed forms (reference analysis.py:202-245) and the
-KvStream container the replay harness consumes (reference stream.py:68-124,
-without the KVTR file format, which is out of scope here)."""
+KvStream container the replay harness consumes (reference stream.py:68-124;
+the KVTR file format and its GPU ingestion live in trace.py)."""
 
 from __future__ import annotations
 

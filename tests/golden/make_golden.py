@@ -281,6 +281,33 @@ def gen_snapshot():
     save("snapshot.npz", **out)
 
 
+def gen_trace():
+    """KVTR images written by the reference (stream.py:126-150) for a small generated stream,
+    fp16 and fp32, and the reference reader's fp64 arrays."""
+    import tempfile
+    from patternkv import stream as rstream
+
+    spec = analysis.SyntheticStreamSpec(
+        layers=2, heads=3, head_dim=16, prefill_len=40, decode_len=12,
+        k_model=analysis.KeyModel(outlier_channels=(3,), outlier_multipliers=(32.0,), drift_rate=1.0 / 52,
+                                  noise_std=0.05),
+        v_model=analysis.ValueModel(cluster_count=8, center_spread=5.0, within_std=0.2, consistency=0.9,
+                                    vocab_size=64),
+        seed=77,
+    )
+    st = analysis.generate_synthetic_stream(spec)
+    out = {"prefill_k": st.prefill_k, "prefill_v": st.prefill_v, "decode_k": st.decode_k, "decode_v": st.decode_v}
+    for code, name in ((1, "f16"), (2, "f32")):
+        with tempfile.NamedTemporaryFile(suffix=".kvtr") as f:
+            rstream.write_trace(f.name, st, dtype_code=code)
+            blob = open(f.name, "rb").read()
+            back = rstream.read_trace(f.name)
+        out[name + "_blob"] = np.frombuffer(blob, np.uint8)
+        out[name + "_read_prefill_k"] = back.prefill_k
+        out[name + "_read_decode_v"] = back.decode_v
+    save("trace.npz", **out)
+
+
 if __name__ == "__main__":
     gen_quant()
     gen_match()
@@ -290,4 +317,5 @@ if __name__ == "__main__":
     gen_engine()
     gen_acceptance()
     gen_snapshot()
+    gen_trace()
     print("golden fixtures written to", HERE)
