@@ -43,12 +43,13 @@ def hbm_peak():
         return HBM_FALLBACK, "fallback"
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
-    (profiles/traffic.json, written by tools/make_profiles.py) or None."""
+def ncu_traffic(kernel: str, token_units: int):
+    """DRAM bytes (read + write) per launch of `kernel` at this run's size: the per-token-unit
+    traffic of the committed ncu --set full capture (profiles/traffic.json, written by
+    tools/make_profiles.py) times the launch's token-units; None without a capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return float(json.load(f)["bytes_per_launch"][kernel])
+            return float(json.load(f)["bytes_per_token_unit"][kernel]) * token_units
     except Exception:
         return None
 
@@ -371,14 +372,14 @@ def main():
                                f"G=W=128", "units_per_gpu": U, "tokens": T, "bits": args.bits,
                    "l2": "inputs 34 GB/GPU >> 126 MB L2 (no flush needed)", "parallelism": f"units x{world}"},
         "roofline": {"bound": "hbm", "achieved": kern_gbps, "peak": peak, "unit": "GB/s",
-                     "frac": kern_gbps / peak, "traffic": ncu_traffic("encode"), "peak_kind": peak_kind,
+                     "frac": kern_gbps / peak, "traffic": ncu_traffic("encode", U * committed), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": r["enc_bytes"],
-                     "kernel": "encode_span_kernel<__half>", "bytes_per_token_unit": r["bpt"]},
+                     "kernel": f"encode_tc_kernel<{args.bits}> (K1-TC)", "bytes_per_token_unit": r["bpt"]},
         "decode_attn": {"tokens_per_s": r["tok_s"], "ms_per_step": r["att_ms"], "GBps": r["att_gbps"],
                         "frac": r["att_gbps"] / peak, "bytes_per_step": r["att_bytes"], "gqa": args.gqa,
                         "context": T, "e2e_ms_per_step": results.get("e2e_attn_ms"),
                         "kernel": "attn_chunk_kernel + attn_merge_kernel", "clocks": r["clk_a"],
-                        "traffic": ncu_traffic("attn")},
+                        "traffic": ncu_traffic("attn", U * committed)},
         "mining": {"ms": r["mine_ms"], "units": min(args.pool, U), "sides": 2, "tokens": T,
                    "patterns": args.patterns,
                    "kernel": "kmeans_kernel<__half, TC>: distance GEMM on tcgen05 (TMA + TMEM), fp64 means/objective"},

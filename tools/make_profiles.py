@@ -52,6 +52,8 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "round1"
     os.makedirs(PROF, exist_ok=True)
     traffic = {}
+    # token-units (units x committed tokens) of the captured launches (tools/gpu_profiles.sh MED config)
+    units = int(os.environ.get("PROF_UNITS", 2 * 32 * 8)) * int(os.environ.get("PROF_COMMITTED", 32768 - 128))
     for name in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn"):
         rep = os.path.join(OUT, name + ".ncu-rep")
         if not os.path.exists(rep):
@@ -65,16 +67,17 @@ def main():
         txt += "\n\nhot source lines (share of executed instructions / of stall samples):\n" + lines(rep)
         with open(os.path.join(PROF, f"{tag}_{name}.txt"), "w") as f:
             f.write(f"# ncu --set full capture: {name}.ncu-rep ({tag})\n\n" + txt)
-        if name.endswith("_full") and "dram__bytes_read.sum" in raw:
+        if name.endswith("_full") and "dram__bytes_read.sum" in raw and "kmeans" not in name:
             def to_bytes(v):
                 val, unit = float(v[0].replace(",", "")), v[1]
                 return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
             traffic[name.replace("prof_", "").replace("_full", "")] = (
-                to_bytes(raw["dram__bytes_read.sum"]) + to_bytes(raw["dram__bytes_write.sum"]))
+                to_bytes(raw["dram__bytes_read.sum"]) + to_bytes(raw["dram__bytes_write.sum"])) / units
     if traffic:
         with open(os.path.join(PROF, "traffic.json"), "w") as f:
-            json.dump({"source": f"ncu --set full, bench configuration ({tag})", "bytes_per_launch": traffic}, f,
-                      indent=1)
+            json.dump({"source": f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum ({tag}), "
+                                 f"per token-unit of the captured launch ({units} token-units)",
+                       "bytes_per_token_unit": traffic}, f, indent=1)
     lp = os.path.join(OUT, "launches.csv")
     if os.path.exists(lp):
         with open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w") as f:
