@@ -280,7 +280,8 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
       dalloc(&d.nk, (size_t)n_units * 4) || dalloc(&d.nv, (size_t)n_units * 4) ||
       dalloc(&d.probe, (size_t)n_units * 2 * 16 * 4) ||
       dalloc(&d.wk, (size_t)n_units * d.Wcap * head_dim * c->esize) ||
-      dalloc(&d.wv, (size_t)n_units * d.Wcap * head_dim * c->esize) || dalloc(&c->scratch_flag, 8))
+      dalloc(&d.wv, (size_t)n_units * d.Wcap * head_dim * c->esize) || dalloc(&c->scratch_flag, 8) ||
+      dalloc(&d.work, 16))
     return bail(fail(PKV_CUDA, -1, "cudaMalloc failed: %s", cudaGetErrorString(cudaGetLastError())));
   if (flags & PKV_FLAG_STATS) {
     if (dalloc(&c->stats, 16)) return bail(fail(PKV_CUDA, -1, "cudaMalloc failed"));
@@ -297,7 +298,7 @@ extern "C" int pkv_cache_destroy(pkv_cache* c) {
   DevCache& d = c->dev;
   void* ptrs[] = {d.kpat64, d.vpat64, d.kpat32, d.vpat32, d.kpmax, d.vpmax, d.nk, d.nv, d.probe, d.blk_start, d.blk_len,
                   d.kcodes, d.kparam32, d.kparam64, d.kidx, d.vcodes, d.vparam32, d.vparam64, d.vidx, d.kdiag,
-                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag};
+                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag, d.work};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;

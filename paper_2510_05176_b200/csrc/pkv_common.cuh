@@ -192,6 +192,7 @@ struct DevCache {
   void* wk; void* wv;
   // stats
   unsigned* stats;                // [0] fp64 refines, [1] exact-division fallbacks
+  int* work;                      // [4] work-queue counters of the K1-TC encoder (reset per launch)
 };
 
 // Source rows for an encode launch: row r of the span that starts `off` rows

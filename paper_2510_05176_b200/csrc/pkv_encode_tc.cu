@@ -40,8 +40,7 @@ namespace fe {
 
 using namespace sm100;
 
-constexpr int NTHR = 512;   // 16 warps: 0-7 K pipeline, 8-15 V pipeline
-constexpr int GT = 256;     // threads per side group
+constexpr int NTHR = 512;   // 16 warps: four 4-warp subgroups, all on the CTA's side (K or V)
 constexpr int PM = 32;      // max patterns per side on this path
 constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23
 #define FE_INF __int_as_float(0x7f800000)
@@ -52,12 +51,16 @@ constexpr float TWO_M17 = 7.62939453125e-06f;
 constexpr float TWO_M22 = 2.384185791015625e-07f;
 
 // ---- shared memory map (bytes from a 1024-aligned base) ---------------------------------
-// Four 4-warp subgroups: K0, K1 (warps 0-7) and V0, V1 (warps 8-15); the two subgroups of
-// a side alternate over the items of each unit and share that side's pattern tables.
+// A CTA works on ONE side at a time: its four 4-warp subgroups (sgi = warp / 4) take turns
+// over the items of a chunk and share the side's pattern tables.  Chunks (<= CHUNK items of
+// one unit) come from a per-side global queue; a CTA starts on its TPC's side (both SMs of a
+// TPC on the same side) and moves to the other side's queue when its own runs dry.  One side
+// per TPC keeps the hot code in the instruction caches: K and V warps on one SM (or TPC)
+// thrash them (~30% of stall samples were no_instruction), a mixed TPC runs ~1.5x slower.
 constexpr int SZ_X = 32768;                       // span tile [2 halves][128 rows][128 B], SW128
-constexpr int OFF_X = 0;                          // X[sgi], sgi = 2*side + sg
+constexpr int OFF_X = 0;                          // X[sgi]
 constexpr int SZ_B = 16384;                       // centered hi [2][32][128 B] then lo [2][32][128 B]
-constexpr int OFF_B = OFF_X + 4 * SZ_X;           // B[side]
+constexpr int OFF_B = OFF_X + 4 * SZ_X;           // B[side] (K CTAs: B[1] holds KW[2], KW[3])
 constexpr int SZ_M = PM * 128 * 4;                // fp32 table, lane-permuted rows (mslot)
 constexpr int OFF_M = OFF_B + 2 * SZ_B;           // M[side]
 constexpr int NSC = 9;                            // scratch arrays of 128 words per subgroup
@@ -65,9 +68,11 @@ constexpr int SZ_SC = NSC * 128 * 4;
 constexpr int OFF_SC = OFF_M + 2 * SZ_M;          // SC[sgi]
 constexpr int SZ_PAT = (4 * 32 + 128 + 4) * 4;    // bb, mn, pm, mabsr [4][32], mabsc[128], flags[4]
 constexpr int OFF_PAT = OFF_SC + 4 * SZ_SC;       // PAT[side]
-constexpr int OFF_BAR = OFF_PAT + 2 * SZ_PAT;     // xfull[4], mma[4], release counters[4], tmem addr
-constexpr int OFF_KW = OFF_BAR + 128;             // 2-bit K code words [2][8 tiles][32 lanes][4]
+constexpr int OFF_BAR = OFF_PAT + 2 * SZ_PAT;     // xfull[4], mma[4], release counters[4], tmem addr,
+                                                  // chunk ring[2] at +96
+constexpr int OFF_KW = OFF_BAR + 128;             // 2-bit K code words KW[0], KW[1]: [8 tiles][32 lanes][4]
 constexpr int SZ_KW = 8 * 32 * 4 * 4;
+static_assert(2 * SZ_KW <= SZ_B, "KW[2..3] live in the unused B[1] of a K CTA");
 __host__ __device__ constexpr int smem_bytes(int bits) { return OFF_KW + (bits == 2 ? 2 * SZ_KW : 0) + 1024; }
 static_assert(smem_bytes(2) <= 232448 && smem_bytes(4) <= 232448, "shared memory budget");
 
@@ -110,9 +115,13 @@ struct Args {
   int64_t unit_stride;   // elements between units
   int64_t nitems;        // U * nb
   double yq;             // RN(1 / qmax)
+  int k_tpc;             // TPCs [0, k_tpc) start on K, the rest on V
+  int chunk;             // items per chunk
+  int cpu;               // chunks per unit
+  int nchunks;           // U * cpu per side
 };
 
-__device__ __forceinline__ void bar_side(int side) { asm volatile("bar.sync %0, %1;" ::"r"(1 + side), "n"(256) : "memory"); }
+__device__ __forceinline__ void bar_side() { asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory"); }
 __device__ __forceinline__ void bar_sub(int sgi) { asm volatile("bar.sync %0, %1;" ::"r"(3 + sgi), "n"(128) : "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
@@ -266,7 +275,7 @@ __device__ __noinline__ int refine64(const unsigned char* X, int t, const double
 }
 // ---------------------------------------------------------------------------------------
 // pattern staging for (unit u, side): permuted fp32 table, centered hi/lo B operand,
-// per-pattern scalars.  Called by the side group between group barriers.
+// per-pattern scalars.  Called by all threads of the CTA between CTA barriers.
 // ---------------------------------------------------------------------------------------
 __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb, int gtid) {
   const DevCache& c = A.c;
@@ -278,7 +287,7 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
   Pat pt(sb, side);
   const int pa = c.probe[((int64_t)u * 2 + side) * 16 + 0], pbc = c.probe[((int64_t)u * 2 + side) * 16 + 1];
   if (gtid == 0) pt.flags()[1] = 0;
-  for (int i = gtid; i < PM * 128; i += GT) {
+  for (int i = gtid; i < PM * 128; i += NTHR) {
     const int p = i >> 7, ch = i & 127;
     M[p * 128 + mpos(p, ch)] = p < P ? p32[(int64_t)p * c.Dp + ch] : 0.f;
   }
@@ -287,11 +296,11 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
     for (int p = 0; p < P; ++p) m = fmaxf(m, fabsf(p32[(int64_t)p * c.Dp + gtid]));
     pt.mabsc()[gtid] = m;
   }
-  bar_side(side);  // flags[1] reset visible
-  // one warp per pattern (8 warps x 4): mean in fp64, centered hi/lo fp16 rows
+  bar_side();  // flags[1] reset visible
+  // one warp per pattern (16 warps x 2): mean in fp64, centered hi/lo fp16 rows
   const int w = gtid >> 5, lane = gtid & 31;
   warp_converged();
-  for (int p = w; p < PM; p += 8) {
+  for (int p = w; p < PM; p += NTHR / 32) {
     double mv[4], s = 0.0;
     float amax = 0.f;
 #pragma unroll
@@ -1036,15 +1045,15 @@ __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, in
 // ---------------------------------------------------------------------------------------
 template <int BITS, int SIDE>
 __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const CUtensorMap* tm, uint32_t tmem,
-                                        int64_t i0, int64_t i1) {
+                                        uint32_t& k) {
   const DevCache& c = A.c;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sg = (warp >> 2) & 1, w = warp & 3, sgi = 2 * SIDE + sg;
-  const int gtid = threadIdx.x & 255, st = 32 * w + lane;
+  const int sg = warp >> 2, w = warp & 3, sgi = sg;
+  const int gtid = threadIdx.x, st = 32 * w + lane;
   unsigned char* X = sb + OFF_X + sgi * SZ_X;
   unsigned char* B = sb + OFF_B + SIDE * SZ_B;
   const float* M = reinterpret_cast<const float*>(sb + OFF_M + SIDE * SZ_M);
-  uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW + sg * SZ_KW);
+  uint32_t* KW = reinterpret_cast<uint32_t*>(sb + (sg < 2 ? OFF_KW + sg * SZ_KW : OFF_B + SZ_B + (sg - 2) * SZ_KW));
   uint64_t* xfull = reinterpret_cast<uint64_t*>(sb + OFF_BAR) + sgi;
   uint64_t* mmab = reinterpret_cast<uint64_t*>(sb + OFF_BAR + 32) + sgi;
   int* rel = reinterpret_cast<int*>(sb + OFF_BAR + 64) + sgi;
@@ -1052,14 +1061,13 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
   Pat pt(sb, SIDE);
   const int nb = A.nb;
   unsigned* stats = c.stats;
-
-  auto first_item = [&](int64_t a) -> int64_t {  // this subgroup's first item at or after unit start a
-    while (a < i1) {
-      const int64_t b = min(i1, (a / nb + 1) * (int64_t)nb);
-      if (a + sg < b) return a + sg;
-      a = b;
-    }
-    return -1;
+  int* ring = reinterpret_cast<int*>(sb + OFF_BAR + 96);
+  auto chunk_items = [&](int ch, int64_t& b0, int64_t& b1) {
+    b0 = b1 = 0;
+    if (ch >= A.nchunks) return;
+    const int uu = ch / A.cpu, pc = ch % A.cpu;
+    b0 = (int64_t)uu * nb + pc * A.chunk;
+    b1 = (int64_t)uu * nb + min(nb, (pc + 1) * A.chunk);
   };
   auto issue = [&](int64_t item) {
     const int uu = (int)(item / nb);
@@ -1070,21 +1078,26 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
     tma_load_3d(X, tm, xfull, 0, row, uu);
     tma_load_3d(X + 16384, tm, xfull, 64, row, uu);
   };
-  if (w == 0 && lane == 0) {
-    const int64_t f = first_item(i0);
-    if (f >= 0) issue(f);
-  }
-  uint32_t k = 0;
-  for (int64_t a = i0; a < i1;) {
-    const int u = (int)(a / nb);
-    const int64_t bend = min(i1, (int64_t)(u + 1) * nb);
-    bar_side(SIDE);
-    stage_patterns(A, SIDE, u, sb, gtid);
-    bar_side(SIDE);
+  int staged = -1;
+  int64_t pending = -1;  // item whose TMA this subgroup already issued
+  for (;;) {
+    const int cur = ring[0], nx = ring[1];
+    if (cur >= A.nchunks) break;
+    int64_t i0, i1, j0, j1;
+    chunk_items(cur, i0, i1);
+    chunk_items(nx, j0, j1);
+    const int u = cur / A.cpu;
+    if (u != staged) {
+      stage_patterns(A, SIDE, u, sb, gtid);
+      bar_side();
+      staged = u;
+    }
     const int P = pt.flags()[0];
     const float pmx = SIDE == 0 ? c.kpmax[u] : c.vpmax[u];
     const double* p64 = (SIDE == 0 ? c.kpat64 : c.vpat64) + (int64_t)u * c.Pcap * 128;
-    for (int64_t it = a + sg; it < bend; it += 2, ++k) {
+    for (int64_t it = i0 + sg; it < i1; it += 4, ++k) {
+      // first item of the chunk not prefetched: every warp is past the chunk barrier, x is free
+      if (pending != it && w == 0 && lane == 0) issue(it);
       const int b = A.first_block + (int)(it % nb);
       const int L = c.blk_len[b];
       const int64_t start = c.blk_start[b];
@@ -1108,7 +1121,8 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         mma_commit(mmab);
       }
       token_stage(SIDE == 1, sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats);
-      const int64_t nxt = it + 2 < bend ? it + 2 : first_item(bend);
+      const int64_t nxt = it + 4 < i1 ? it + 4 : (j0 + sg < j1 ? j0 + sg : -1);
+      pending = nxt;
       if constexpr (SIDE == 0) {
         bar_sub(sgi);  // every token's final pattern index
         if (st < L) c.kidx[blk * c.GP + st] = (int16_t)sc.fidx()[st];
@@ -1172,7 +1186,12 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         }
       }
     }
-    a = bend;
+    bar_side();  // every subgroup is done with chunk cur and the pattern tables
+    if (gtid == 0) {
+      ring[0] = nx;
+      ring[1] = atomicAdd(&c.work[SIDE], 1);
+    }
+    bar_side();
   }
 }
 
@@ -1186,10 +1205,10 @@ encode_tc_kernel(const Args A, const __grid_constant__ CUtensorMap tmK, const __
   uint64_t* bars = reinterpret_cast<uint64_t*>(sb + OFF_BAR);
   int* rel = reinterpret_cast<int*>(sb + OFF_BAR + 64);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sb + OFF_BAR + 80);
-  if (BITS == 2) {
-    uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW);
-    for (int i = tid; i < 2 * SZ_KW / 4; i += NTHR) KW[i] = 0u;
-  }
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  int side = (int)(smid >> 1) < A.k_tpc ? 0 : 1;
+  int* ring = reinterpret_cast<int*>(sb + OFF_BAR + 96);
   if (tid < 4) rel[tid] = 0;
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
@@ -1202,11 +1221,22 @@ encode_tc_kernel(const Args A, const __grid_constant__ CUtensorMap tmK, const __
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const int64_t per = A.nitems / gridDim.x, rem = A.nitems % gridDim.x;
-  const int64_t i0 = (int64_t)blockIdx.x * per + min((int64_t)blockIdx.x, rem);
-  const int64_t i1 = i0 + per + ((int64_t)blockIdx.x < rem ? 1 : 0);
-  if (warp < 8) run_sub<BITS, 0>(A, sb, &tmK, tmem, i0, i1);
-  else run_sub<BITS, 1>(A, sb, &tmV, tmem, i0, i1);
+  uint32_t k = 0;  // items this subgroup processed (mbarrier phases), across both sides
+  for (int pass = 0; pass < 2; ++pass, side ^= 1) {
+    if (BITS == 2 && side == 0) {  // K code words start zeroed (KW[2..3] alias the V side's B)
+      uint32_t* KW = reinterpret_cast<uint32_t*>(sb + OFF_KW);
+      uint32_t* KW2 = reinterpret_cast<uint32_t*>(sb + OFF_B + SZ_B);
+      for (int i = tid; i < 2 * SZ_KW / 4; i += NTHR) KW[i] = KW2[i] = 0u;
+    }
+    if (tid == 0) {
+      ring[0] = atomicAdd(&A.c.work[side], 1);
+      ring[1] = atomicAdd(&A.c.work[side], 1);
+    }
+    __syncthreads();
+    if (side == 0) run_sub<BITS, 0>(A, sb, &tmK, tmem, k);
+    else run_sub<BITS, 1>(A, sb, &tmV, tmem, k);
+    __syncthreads();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1272,7 +1302,27 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const int grid = (int)std::min<int64_t>(nsm, a.nitems);
+  // starting sides: K costs ~2.6x V per item, so ~72% of the TPCs start on K; the queues
+  // balance the rest (a CTA whose side runs dry takes the other side's chunks)
+  static double kfrac = 0.0;
+  if (kfrac <= 0.0) {
+    const char* kf = getenv("PKV_TC_KFRAC");
+    kfrac = kf ? atof(kf) : 0.72;
+    if (!(kfrac > 0.0 && kfrac < 1.0)) kfrac = 0.72;
+  }
+  static int chunk = 0;
+  if (!chunk) {
+    const char* ce = getenv("PKV_TC_CHUNK");
+    chunk = ce ? atoi(ce) : 16;
+    if (chunk < 4 || chunk > 4096) chunk = 16;
+  }
+  a.k_tpc = (int)(kfrac * (nsm / 2) + 0.5);
+  a.chunk = chunk;
+  a.cpu = (nblocks + chunk - 1) / chunk;
+  if ((int64_t)c.U * a.cpu + 2 * nsm >= (1ll << 31)) return cudaErrorNotSupported;
+  a.nchunks = c.U * a.cpu;
+  const int grid = (int)std::min<int64_t>(nsm, 2 * (int64_t)a.nchunks);
+  if (cudaMemsetAsync(c.work, 0, 16, st) != cudaSuccess) return cudaGetLastError();
   if (c.bits == 2) {
     cudaFuncSetAttribute(fe::encode_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::smem_bytes(2));
     fe::encode_tc_kernel<2><<<grid, fe::NTHR, fe::smem_bytes(2), st>>>(a, tk, tv);
