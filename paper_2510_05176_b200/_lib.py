@@ -13,7 +13,7 @@ import os
 from .errors import DataError, UsageError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpkv_b200.so")
+LIB_PATH = os.environ.get("PKV_LIB") or os.path.join(_HERE, "libpkv_b200.so")  # PKV_LIB: A/B builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

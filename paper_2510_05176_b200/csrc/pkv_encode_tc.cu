@@ -1069,10 +1069,11 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
     b0 = (int64_t)uu * nb + pc * A.chunk;
     b1 = (int64_t)uu * nb + min(nb, (pc + 1) * A.chunk);
   };
+  const int64_t row0 = c.blk_start[A.first_block];
   auto issue = [&](int64_t item) {
     const int uu = (int)(item / nb);
     const int bb = A.first_block + (int)(item % nb);
-    const int row = (int)(c.blk_start[bb] - c.blk_start[A.first_block]);
+    const int row = (int)(c.blk_start[bb] - row0);
     fence_proxy_async();
     mbar_arrive_expect_tx(xfull, 2 * 16384);
     tma_load_3d(X, tm, xfull, 0, row, uu);
@@ -1099,12 +1100,13 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
       // first item of the chunk not prefetched: every warp is past the chunk barrier, x is free
       if (pending != it && w == 0 && lane == 0) issue(it);
       const int b = A.first_block + (int)(it % nb);
-      const int L = c.blk_len[b];
-      const int64_t start = c.blk_start[b];
-      const __half* xsrc = A.src[SIDE] + (int64_t)u * A.unit_stride + (start - c.blk_start[A.first_block]) * 128;
-      const int64_t blk = (int64_t)u * c.NBcap + b;
       const uint32_t ph = k & 1;
       const uint32_t tcol = tmem + sgi * 64 + ph * 32;
+      // span metadata: loads issued before the x wait, consumed after the token stage
+      int L;
+      int64_t start;
+      asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(L) : "l"(c.blk_len + b));
+      asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(start) : "l"(c.blk_start + b));
       mbar_wait(xfull, ph);
       if (w == 0 && lane == 0) {
         tc_fence_after();
@@ -1121,6 +1123,8 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         mma_commit(mmab);
       }
       token_stage(SIDE == 1, sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats);
+      const __half* xsrc = A.src[SIDE] + (int64_t)u * A.unit_stride + (start - row0) * 128;
+      const int64_t blk = (int64_t)u * c.NBcap + b;
       const int64_t nxt = it + 4 < i1 ? it + 4 : (j0 + sg < j1 ? j0 + sg : -1);
       pending = nxt;
       if constexpr (SIDE == 0) {
