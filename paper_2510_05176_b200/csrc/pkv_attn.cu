@@ -215,13 +215,28 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
     int ki0, ki1, vi0, vi1;
     float2 vp0, vp1;
   };
-  auto load_tile = [&](int bb, int ti, Tile& t) {
-    const int64_t bo = (int64_t)u * c.NBcap + bb;
-    const uint8_t* kt = c.kcodes + bo * c.blk_bytes + (size_t)ti * tbytes;
-    const uint8_t* vt = c.vcodes + bo * c.blk_bytes + (size_t)ti * tbytes;
-    load_words<BITS>(kt, lane, t.kw, WL);
-    load_words<BITS>(vt, lane, t.vw, WL);
-    const int64_t slot = bo * c.GP + 16 * ti + g;
+  // per-block base: the block offset, and at 2 bits (where registers allow) the code pointers,
+  // so the per-tile address work is a few adds
+  struct BlkPtr {
+    int64_t bo;
+    const uint8_t* k;
+    const uint8_t* v;
+  };
+  auto blk_ptr = [&](int bb) {
+    BlkPtr p;
+    p.bo = (int64_t)u * c.NBcap + bb;
+    if constexpr (BITS == 2) {
+      p.k = c.kcodes + p.bo * c.blk_bytes;
+      p.v = c.vcodes + p.bo * c.blk_bytes;
+    }
+    return p;
+  };
+  auto load_tile = [&](const BlkPtr& bp, int ti, Tile& t) {
+    const uint8_t* kb = BITS == 2 ? bp.k : c.kcodes + bp.bo * c.blk_bytes;
+    const uint8_t* vb = BITS == 2 ? bp.v : c.vcodes + bp.bo * c.blk_bytes;
+    load_words<BITS>(kb + ti * tbytes, lane, t.kw, WL);
+    load_words<BITS>(vb + ti * tbytes, lane, t.vw, WL);
+    const int64_t slot = bp.bo * c.GP + g + 16 * ti;
     t.ki0 = __ldg(c.kidx + slot); t.ki1 = __ldg(c.kidx + slot + 8);
     t.vi0 = __ldg(c.vidx + slot); t.vi1 = __ldg(c.vidx + slot + 8);
     t.vp0 = __ldg(reinterpret_cast<const float2*>(c.vparam32) + slot);
@@ -275,17 +290,22 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
 
   int b = b0 + warp, ti = 0;
   Tile ta, tb;
+  BlkPtr bp{};  // current block of this warp
+  int L = 0;
   if (b < b1) {
-    load_tile(b, 0, ta);
+    bp = blk_ptr(b);
+    L = __ldg(c.blk_len + b);
+    load_tile(bp, 0, ta);
     block_setup(b);
   }
   // one tile of block b (state cur), prefetching the next tile of the warp into nxt
   auto step = [&](Tile& cur, Tile& nxt) {
-    const int L = c.blk_len[b];
     const int ntile = (L + 15) >> 4;
-    int nb2 = b, nti = ti + 1;
-    if (nti >= ntile) { nb2 = b + ATT_WARPS; nti = 0; }
-    if (nb2 < b1) load_tile(nb2, nti, nxt);  // prefetch while this tile computes
+    int nti = ti + 1;
+    const bool nextblk = nti >= ntile;
+    if (nextblk) nti = 0;
+    if (!nextblk) load_tile(bp, nti, nxt);  // prefetch while this tile computes
+    else if (b + ATT_WARPS < b1) load_tile(blk_ptr(b + ATT_WARPS), 0, nxt);
     const int r0 = 16 * ti + g, r1 = r0 + 8;
     const bool ok0 = r0 < L, ok1 = r1 < L;
     const int vi0 = ok0 ? cur.vi0 : -1, vi1 = ok1 ? cur.vi1 : -1;
@@ -377,9 +397,13 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
       }
     }
     ti = nti;
-    if (nb2 != b) {
-      b = nb2;
-      if (b < b1) block_setup(b);
+    if (nextblk) {
+      b += ATT_WARPS;
+      if (b < b1) {
+        bp = blk_ptr(b);
+        L = __ldg(c.blk_len + b);
+        block_setup(b);
+      }
     }
   };
   while (b < b1) {
