@@ -44,6 +44,7 @@ from .patterns import (
 )
 from .quant import QuantizedGroup, QuantParams, dequantize_group, pack_codes, quantize_group, unpack_codes
 from .trace import TraceHeader, ingest_trace, load_trace_device, read_trace, read_trace_header, write_trace
+from . import verify
 from .snapshot import (
     SNAPSHOT_MAGIC,
     SNAPSHOT_VERSION,
@@ -66,5 +67,5 @@ __all__ = [
     "minmax_distance", "reconstruct_vector", "QuantizedGroup", "QuantParams", "dequantize_group", "pack_codes",
     "quantize_group", "unpack_codes", "SNAPSHOT_MAGIC", "SNAPSHOT_VERSION", "save_snapshot", "load_snapshot",
     "save_cache_snapshot", "cache_snapshot_bytes", "restore_cache", "TraceHeader", "write_trace", "read_trace",
-    "read_trace_header", "load_trace_device", "ingest_trace",
+    "read_trace_header", "load_trace_device", "ingest_trace", "verify",
 ]

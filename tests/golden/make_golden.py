@@ -308,6 +308,30 @@ def gen_trace():
     save("trace.npz", **out)
 
 
+def gen_analysis():
+    """variance_decomposition / covering_bound_check instances (the verify suites' host checks)."""
+    import dataclasses
+
+    rng = np.random.default_rng(2024)
+    out = {}
+    n = 40
+    for i in range(n):
+        t = int(rng.integers(2, 120))
+        d = int(rng.integers(1, 6))
+        k = int(rng.integers(1, 8))
+        pts = rng.normal(0.0, 10.0 ** rng.uniform(-2, 2), size=(t, d)) + rng.uniform(-50, 50)
+        if i == n - 1:  # the diagonal set: zero width radius
+            pts = np.outer(np.linspace(-3, 3, 17), np.ones(3)) + 0.5
+        lab = rng.integers(0, k, size=pts.shape[0])
+        rho = float(rng.uniform(0.2, 0.9))
+        rep = analysis.variance_decomposition(pts, lab, group_count=k)
+        cov = analysis.covering_bound_check(pts, rho, bits=2)
+        out.update({f"pts{i}": pts, f"lab{i}": lab, f"k{i}": k, f"rho{i}": rho, f"total{i}": rep.total,
+                    f"intra{i}": rep.intra, f"inter{i}": rep.inter,
+                    f"cov{i}": np.array(dataclasses.astuple(cov), dtype=np.float64)})
+    save("analysis.npz", n=n, **out)
+
+
 if __name__ == "__main__":
     gen_quant()
     gen_match()
@@ -318,4 +342,5 @@ if __name__ == "__main__":
     gen_acceptance()
     gen_snapshot()
     gen_trace()
+    gen_analysis()
     print("golden fixtures written to", HERE)
