@@ -66,7 +66,7 @@ constexpr int OFF_M = OFF_B + 2 * SZ_B;           // M[side]
 constexpr int NSC = 9;                            // scratch arrays of 128 words per subgroup
 constexpr int SZ_SC = NSC * 128 * 4;
 constexpr int OFF_SC = OFF_M + 2 * SZ_M;          // SC[sgi]
-constexpr int SZ_PAT = (4 * 32 + 128 + 4) * 4;    // bb, mn, pm, mabsr [4][32], mabsc[128], flags[4]
+constexpr int SZ_PAT = (4 * 32 + 128 + 8 + 4 * 32) * 4;  // bb, mn, pm, mabsr [4][32], mabsc[128], flags[8], pm4[32][4]
 constexpr int OFF_PAT = OFF_SC + 4 * SZ_SC;       // PAT[side]
 constexpr int OFF_BAR = OFF_PAT + 2 * SZ_PAT;     // xfull[4], mma[4], release counters[4], tmem addr,
                                                   // chunk ring[2] at +96
@@ -101,10 +101,11 @@ struct Pat {   // per-side pattern scalars
   __device__ explicit Pat(unsigned char* sb, int side) : base(sb + OFF_PAT + side * SZ_PAT) {}
   __device__ float* bb() const { return reinterpret_cast<float*>(base); }            // ||m'_p||^2 (+inf past P)
   __device__ float* mn() const { return reinterpret_cast<float*>(base + 128); }      // ||m'_p||
-  __device__ float* pm() const { return reinterpret_cast<float*>(base + 256); }      // m_a - m_b (probe pair)
+  __device__ float* pm() const { return reinterpret_cast<float*>(base + 256); }      // (unused)
+  __device__ float* pm4() const { return reinterpret_cast<float*>(base + 1056); }    // K: m32 at the 4 probe channels
   __device__ float* mabsr() const { return reinterpret_cast<float*>(base + 384); }   // max_c |m_pc|
   __device__ float* mabsc() const { return reinterpret_cast<float*>(base + 512); }   // max_p |m_pc| (K)
-  __device__ int* flags() const { return reinterpret_cast<int*>(base + 1024); }      // P, no-L2, probe a, b
+  __device__ int* flags() const { return reinterpret_cast<int*>(base + 1024); }      // P, no-L2, probe channels [2..5]
 };
 
 struct Args {
@@ -285,7 +286,7 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
   float* M = reinterpret_cast<float*>(sb + OFF_M + side * SZ_M);
   unsigned char* B = sb + OFF_B + side * SZ_B;
   Pat pt(sb, side);
-  const int pa = c.probe[((int64_t)u * 2 + side) * 16 + 0], pbc = c.probe[((int64_t)u * 2 + side) * 16 + 1];
+  const int* prb = c.probe + ((int64_t)u * 2 + side) * 16;  // channels by pattern spread (probe_kernel)
   if (gtid == 0) pt.flags()[1] = 0;
   for (int i = gtid; i < PM * 128; i += NTHR) {
     const int p = i >> 7, ch = i & 127;
@@ -332,14 +333,18 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
     if (lane == 0) {
       pt.bb()[p] = p < P ? (float)ss : FE_INF;
       pt.mn()[p] = p < P ? (float)sqrt(ss) : 0.f;
-      pt.pm()[p] = p < P ? (float)__dsub_rn(p64[(int64_t)p * 128 + pa], p64[(int64_t)p * 128 + pbc]) : 0.f;
+      if (side == 0)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pt.pm4()[4 * p + j] = p < P ? (float)p64[(int64_t)p * 128 + prb[j]] : 0.f;
       pt.mabsr()[p] = amax;
     }
   }
   if (gtid == 0) {
     pt.flags()[0] = P;
-    pt.flags()[2] = pa;
-    pt.flags()[3] = pbc;
+    pt.flags()[2] = prb[0];
+    pt.flags()[3] = prb[1];
+    pt.flags()[4] = prb[2];
+    pt.flags()[5] = prb[3];
   }
   fence_proxy_async();  // generic-proxy writes of B -> tensor-core reads
 }
@@ -538,7 +543,8 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
 // bounds, survivors, fp64 re-match.  Leaves the final pattern index in sc.fidx() and the
 // keyed statistics of the final residual in sc.kmx()/kmn/xmx/xmn(/info).
 // ---------------------------------------------------------------------------------------
-__device__ __noinline__ void token_stage(bool vs, Scr sc, Pat pt, const unsigned char* X, const float* M,
+template <int SIDE>
+__device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X, const float* M,
                                          uint64_t* mmab, uint32_t ph, uint32_t tcol, int w, int lane, int P, float pmx,
                                          const double* p64, unsigned* stats) {
   SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base);
@@ -565,45 +571,61 @@ __device__ __noinline__ void token_stage(bool vs, Scr sc, Pat pt, const unsigned
   int guess = (int)(__float_as_uint(best) & 31u);
   if (guess >= P) guess = 0;
   const float Cg = best;
-  const float px = __fsub_rn(xt_at(X, tt_, pt.flags()[2]), xt_at(X, tt_, pt.flags()[3]));
+  float x4[4];  // K: x at the 4 probe channels
+  if constexpr (SIDE == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x4[j] = xt_at(X, tt_, pt.flags()[2 + j]);
+  }
   sc.guess()[tt_] = guess;
   __syncwarp();
   // ---- B. keyed residual extrema against the guess, per 16-token tile -----------------
 #pragma unroll 1
   for (int tile = 0; tile < 2; ++tile) {
     const int tb = 32 * w + 16 * tile;
-    if (vs) b_tile<true>(X, M, pt, sc, tb, lane, sc.guess()[tb + g], sc.guess()[tb + g + 8]);
-    else b_tile<false>(X, M, pt, sc, tb, lane, sc.guess()[tb + g], sc.guess()[tb + g + 8]);
+    b_tile<SIDE == 1>(X, M, pt, sc, tb, lane, sc.guess()[tb + g], sc.guess()[tb + g + 8]);
   }
   __syncwarp();
-  // ---- C. prune every other pattern by exact lower bounds (thread per token) ----------
+  // ---- C. prune every other pattern by an exact lower bound (thread per token) --------
+  // K: the range of the residual over the 4 widest-spread channels (d_mm >= that range;
+  //    the Popoviciu bound rarely prunes K).  V: Popoviciu from the GEMM.
   {
     const float kx = sc.kmx()[tt_], kn = sc.kmn()[tt_];
     const float dg = __fsub_rn(kx, kn), xa = fmaxf(fabsf(sc.xmx()[tt_]), fabsf(sc.xmn()[tt_]));
     const float T2 = derr(kx, kn, pt.mabsr()[guess]);  // >= |dg - d64(guess)|
     const float dhi = __fadd_rn(dg, T2) * 1.0000002f;
-    const float dlo = fmaxf(__fsub_rn(dg, T2), 0.f) * 0.9999998f;
-    // Popoviciu: osc^2 >= 4 C / d; C_q >= C'_q - C'_g + C_g, C_g >= osc_g^2 / 2
-    const float theta = __fmaf_rn(32.f * dhi, dhi, -0.5f * dlo * dlo) * 1.000001f;
-    const float kap = TWO_M13 * 11.3137085f * xa;  // 2 x (tensor-core + split error) / ||m'||, ||x|| <= sqrt(d) |x|max
-    const float rhs = theta + Cg + kap * pt.mn()[guess] + TWO_M17 * fabsf(Cg);
-    const bool nol2 = pt.flags()[1] != 0;
-    const float pb = __fadd_rn(dhi, 4.76837158203125e-07f * (xa + pmx));  // probe: 2^-21 (|x| + |m|) rounding
     uint32_t mask = 0;
+    if constexpr (SIDE == 0) {
+      // |r32 - r64| <= 2^-23 (|x| + |m|) per probe residual, + 2^-24 relative on the range:
+      // inside the 2^-21 (|x|max + |m|max) slack
+      const float pb = __fadd_rn(dhi, 4.76837158203125e-07f * (xa + pmx));
+#pragma unroll 4
+      for (int p = 0; p < 32; ++p) {
+        const float4 m4 = *reinterpret_cast<const float4*>(pt.pm4() + 4 * p);
+        const float r0 = __fsub_rn(x4[0], m4.x), r1 = __fsub_rn(x4[1], m4.y);
+        const float r2 = __fsub_rn(x4[2], m4.z), r3 = __fsub_rn(x4[3], m4.w);
+        const float rng = __fsub_rn(fmaxf(fmax3(r0, r1, r2), r3), fminf(fmin3(r0, r1, r2), r3));
+        mask |= (uint32_t)(rng <= pb && p < P) << p;
+      }
+    } else {
+      const float dlo = fmaxf(__fsub_rn(dg, T2), 0.f) * 0.9999998f;
+      // Popoviciu: osc^2 >= 4 C / d; C_q >= C'_q - C'_g + C_g, C_g >= osc_g^2 / 2
+      const float theta = __fmaf_rn(32.f * dhi, dhi, -0.5f * dlo * dlo) * 1.000001f;
+      const float kap = TWO_M13 * 11.3137085f * xa;  // 2 x (tensor-core + split error) / ||m'||, ||x|| <= sqrt(d) |x|max
+      const float rhs = theta + Cg + kap * pt.mn()[guess] + TWO_M17 * fabsf(Cg);
+      const bool nol2 = pt.flags()[1] != 0;
 #pragma unroll 1
-    for (int p0 = 0; p0 < 32; p0 += 8) {
-      uint32_t v[8];
-      tmem_ld8(tl + p0, v);
-      tmem_ld_wait();
+      for (int p0 = 0; p0 < 32; p0 += 8) {
+        uint32_t v[8];
+        tmem_ld8(tl + p0, v);
+        tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int p = p0 + i;
-        const float bbp = pt.bb()[p];
-        const float cp = __fmaf_rn(-2.f, __uint_as_float(v[i]), bbp);
-        const float lhs = __fmaf_rn(-TWO_M22, bbp, __fmaf_rn(-kap, pt.mn()[p], __fmaf_rn(-TWO_M17, fabsf(cp), cp)));
-        const bool l2ok = nol2 || !(lhs > rhs);
-        const bool prok = fabsf(__fsub_rn(px, pt.pm()[p])) <= pb;
-        mask |= (uint32_t)(l2ok && prok && p < P) << p;
+        for (int i = 0; i < 8; ++i) {
+          const int p = p0 + i;
+          const float bbp = pt.bb()[p];
+          const float cp = __fmaf_rn(-2.f, __uint_as_float(v[i]), bbp);
+          const float lhs = __fmaf_rn(-TWO_M22, bbp, __fmaf_rn(-kap, pt.mn()[p], __fmaf_rn(-TWO_M17, fabsf(cp), cp)));
+          mask |= (uint32_t)((nol2 || !(lhs > rhs)) && p < P) << p;
+        }
       }
     }
     tc_fence_before();
@@ -665,8 +687,7 @@ __device__ __noinline__ void token_stage(bool vs, Scr sc, Pat pt, const unsigned
       }
       // statistics of the final residual where the winner moved
       if (__any_sync(0xffffffffu, idx[0] != gi[0] || idx[1] != gi[1])) {
-        if (vs) b_tile<true>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
-        else b_tile<false>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
+        b_tile<SIDE == 1>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
       }
     }
     if (q == 0) { sc.fidx()[t0] = idx[0]; sc.fidx()[t0 + 8] = idx[1]; }
@@ -1122,7 +1143,7 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         }
         mma_commit(mmab);
       }
-      token_stage(SIDE == 1, sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats);
+      token_stage<SIDE>(sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats);
       const __half* xsrc = A.src[SIDE] + (int64_t)u * A.unit_stride + (start - row0) * 128;
       const int64_t blk = (int64_t)u * c.NBcap + b;
       const int64_t nxt = it + 4 < i1 ? it + 4 : (j0 + sg < j1 ? j0 + sg : -1);
