@@ -66,7 +66,9 @@ constexpr int OFF_M = OFF_B + 2 * SZ_B;           // M[side]
 constexpr int NSC = 9;                            // scratch arrays of 128 words per subgroup
 constexpr int SZ_SC = NSC * 128 * 4;
 constexpr int OFF_SC = OFF_M + 2 * SZ_M;          // SC[sgi]
-constexpr int SZ_PAT = (4 * 32 + 128 + 8 + 4 * 32) * 4;  // bb, mn, pm, mabsr [4][32], mabsc[128], flags[8], pm4[32][4]
+constexpr int NPRB = 8;    // K probe channels of the pruning bound
+constexpr int NFLAG = (2 + NPRB + 3) / 4 * 4;      // P, no-L2, probe channels
+constexpr int SZ_PAT = (4 * 32 + 128 + NFLAG + NPRB * 32) * 4;  // bb, mn, pm, mabsr [4][32], mabsc[128], flags, pm4[32][NPRB]
 constexpr int OFF_PAT = OFF_SC + 4 * SZ_SC;       // PAT[side]
 constexpr int OFF_BAR = OFF_PAT + 2 * SZ_PAT;     // xfull[4], mma[4], release counters[4], tmem addr,
                                                   // chunk ring[2] at +96
@@ -102,7 +104,7 @@ struct Pat {   // per-side pattern scalars
   __device__ float* bb() const { return reinterpret_cast<float*>(base); }            // ||m'_p||^2 (+inf past P)
   __device__ float* mn() const { return reinterpret_cast<float*>(base + 128); }      // ||m'_p||
   __device__ float* pm() const { return reinterpret_cast<float*>(base + 256); }      // (unused)
-  __device__ float* pm4() const { return reinterpret_cast<float*>(base + 1056); }    // K: m32 at the 4 probe channels
+  __device__ float* pm4() const { return reinterpret_cast<float*>(base + 1024 + 4 * NFLAG); }  // K: m32 at the probe channels
   __device__ float* mabsr() const { return reinterpret_cast<float*>(base + 384); }   // max_c |m_pc|
   __device__ float* mabsc() const { return reinterpret_cast<float*>(base + 512); }   // max_p |m_pc| (K)
   __device__ int* flags() const { return reinterpret_cast<int*>(base + 1024); }      // P, no-L2, probe channels [2..5]
@@ -335,16 +337,14 @@ __device__ void stage_patterns(const Args& A, int side, int u, unsigned char* sb
       pt.mn()[p] = p < P ? (float)sqrt(ss) : 0.f;
       if (side == 0)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pt.pm4()[4 * p + j] = p < P ? (float)p64[(int64_t)p * 128 + prb[j]] : 0.f;
+        for (int j = 0; j < NPRB; ++j) pt.pm4()[NPRB * p + j] = p < P ? (float)p64[(int64_t)p * 128 + prb[j]] : 0.f;
       pt.mabsr()[p] = amax;
     }
   }
   if (gtid == 0) {
     pt.flags()[0] = P;
-    pt.flags()[2] = prb[0];
-    pt.flags()[3] = prb[1];
-    pt.flags()[4] = prb[2];
-    pt.flags()[5] = prb[3];
+#pragma unroll
+    for (int j = 0; j < NPRB; ++j) pt.flags()[2 + j] = prb[j];
   }
   fence_proxy_async();  // generic-proxy writes of B -> tensor-core reads
 }
@@ -571,10 +571,10 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
   int guess = (int)(__float_as_uint(best) & 31u);
   if (guess >= P) guess = 0;
   const float Cg = best;
-  float x4[4];  // K: x at the 4 probe channels
+  float x4[NPRB];  // K: x at the probe channels
   if constexpr (SIDE == 0) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) x4[j] = xt_at(X, tt_, pt.flags()[2 + j]);
+    for (int j = 0; j < NPRB; ++j) x4[j] = xt_at(X, tt_, pt.flags()[2 + j]);
   }
   sc.guess()[tt_] = guess;
   __syncwarp();
@@ -586,7 +586,7 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
   }
   __syncwarp();
   // ---- C. prune every other pattern by an exact lower bound (thread per token) --------
-  // K: the range of the residual over the 4 widest-spread channels (d_mm >= that range;
+  // K: the range of the residual over the NPRB widest-spread channels (d_mm >= that range;
   //    the Popoviciu bound rarely prunes K).  V: Popoviciu from the GEMM.
   {
     const float kx = sc.kmx()[tt_], kn = sc.kmn()[tt_];
@@ -600,10 +600,16 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
       const float pb = __fadd_rn(dhi, 4.76837158203125e-07f * (xa + pmx));
 #pragma unroll 4
       for (int p = 0; p < 32; ++p) {
-        const float4 m4 = *reinterpret_cast<const float4*>(pt.pm4() + 4 * p);
-        const float r0 = __fsub_rn(x4[0], m4.x), r1 = __fsub_rn(x4[1], m4.y);
-        const float r2 = __fsub_rn(x4[2], m4.z), r3 = __fsub_rn(x4[3], m4.w);
-        const float rng = __fsub_rn(fmaxf(fmax3(r0, r1, r2), r3), fminf(fmin3(r0, r1, r2), r3));
+        float hi = -FE_INF, lo = FE_INF;
+#pragma unroll
+        for (int j = 0; j < NPRB; j += 4) {
+          const float4 m4 = *reinterpret_cast<const float4*>(pt.pm4() + NPRB * p + j);
+          const float r0 = __fsub_rn(x4[j], m4.x), r1 = __fsub_rn(x4[j + 1], m4.y);
+          const float r2 = __fsub_rn(x4[j + 2], m4.z), r3 = __fsub_rn(x4[j + 3], m4.w);
+          hi = fmaxf(hi, fmax3(r0, r1, r2)); hi = fmaxf(hi, r3);
+          lo = fminf(lo, fmin3(r0, r1, r2)); lo = fminf(lo, r3);
+        }
+        const float rng = __fsub_rn(hi, lo);
         mask |= (uint32_t)(rng <= pb && p < P) << p;
       }
     } else {
