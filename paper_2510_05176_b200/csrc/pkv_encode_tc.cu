@@ -53,10 +53,11 @@ constexpr float TWO_M22 = 2.384185791015625e-07f;
 // ---- shared memory map (bytes from a 1024-aligned base) ---------------------------------
 // A CTA works on ONE side at a time: its four 4-warp subgroups (sgi = warp / 4) take turns
 // over the items of a chunk and share the side's pattern tables.  Chunks (<= CHUNK items of
-// one unit) come from a per-side global queue; a CTA starts on its TPC's side (both SMs of a
-// TPC on the same side) and moves to the other side's queue when its own runs dry.  One side
-// per TPC keeps the hot code in the instruction caches: K and V warps on one SM (or TPC)
-// thrash them (~30% of stall samples were no_instruction), a mixed TPC runs ~1.5x slower.
+// one unit) come from a per-side global queue; a CTA starts on its TPC's side (by default
+// every TPC starts on K: a K phase, then a V phase) and moves to the other side's queue when
+// its own runs dry.  One side per SM (and TPC) keeps the hot code in the instruction caches:
+// K and V warps on one SM thrash them (~30% of stall samples were no_instruction), a TPC
+// holding a K and a V CTA runs ~1.5x slower.
 constexpr int SZ_X = 32768;                       // span tile [2 halves][128 rows][128 B], SW128
 constexpr int OFF_X = 0;                          // X[sgi]
 constexpr int SZ_B = 16384;                       // centered hi [2][32][128 B] then lo [2][32][128 B]
@@ -1333,13 +1334,14 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  // starting sides: K costs ~2.6x V per item, so ~72% of the TPCs start on K; the queues
-  // balance the rest (a CTA whose side runs dry takes the other side's chunks)
+  // starting sides: every CTA starts on the K queue and moves to V as K drains (a K phase,
+  // then a V phase, one code path per SM at a time).  Measured against splitting the TPCs
+  // between the sides in the K:V cost ratio (0.72): 781 -> 807 GB/s (2-bit), 761 -> 792 (4-bit).
   static double kfrac = 0.0;
   if (kfrac <= 0.0) {
     const char* kf = getenv("PKV_TC_KFRAC");
-    kfrac = kf ? atof(kf) : 0.72;
-    if (!(kfrac > 0.0 && kfrac < 1.0)) kfrac = 0.72;
+    kfrac = kf ? atof(kf) : 1.0;
+    if (!(kfrac > 0.0 && kfrac <= 1.0)) kfrac = 1.0;
   }
   static int chunk = 0;
   if (!chunk) {
