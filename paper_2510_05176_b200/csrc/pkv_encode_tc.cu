@@ -439,12 +439,10 @@ __device__ __forceinline__ float qmin4(float v) {
   v = fminf(v, __shfl_xor_sync(0xffffffffu, v, 1));
   return fminf(v, __shfl_xor_sync(0xffffffffu, v, 2));
 }
-// count of the two window tests as a negative number: set.*.s32 gives 0 / -1, one IADD3 per element
-__device__ __forceinline__ int win2(float key, float hib, float lob) {
-  int a, b;
-  asm("set.ge.s32.f32 %0, %1, %2;" : "=r"(a) : "f"(key), "f"(hib));
-  asm("set.le.s32.f32 %0, %1, %2;" : "=r"(b) : "f"(key), "f"(lob));
-  return a + b;
+// cnt += (key >= hib || key <= lob): two compares into one predicate and a predicated add
+__device__ __forceinline__ void win_or(int& cnt, float key, float hib, float lob) {
+  asm("{\n .reg .pred p;\n setp.ge.f32 p, %1, %2;\n setp.le.or.f32 p, %1, %3, p;\n @p add.s32 %0, %0, 1;\n}"
+      : "+r"(cnt) : "f"(key), "f"(hib), "f"(lob));
 }
 // bound on |d32 - d64| for a distance taken from keyed fp32 extrema (K1-TC):
 // key error 2^-18 |r|, fp32 residual error 2^-24 (|r| + 2|m|), subtraction 2^-24 |d|
@@ -516,14 +514,14 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          cnt -= win2(fkey(r[h][j][e], 4 * j + e, 0xffffffe0u), hib, lob);
+          win_or(cnt, fkey(r[h][j][e], 4 * j + e, 0xffffffe0u), hib, lob);
         }
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
       const uint32_t gm = 0xfu << (4 * g);
       const uint32_t bmx = __ballot_sync(0xffffffffu, st.kmx[h] == kx) & gm;
       const uint32_t bmn = __ballot_sync(0xffffffffu, st.kmn[h] == kn) & gm;
-      if (cnt == 2 && __popc(bmx) == 1 && __popc(bmn) == 1) {
+      if (cnt == 2 && hib > lob && __popc(bmx) == 1 && __popc(bmn) == 1) {  // disjoint windows
         const int qx = (__ffs(bmx) - 1) & 3, qn = (__ffs(bmn) - 1) & 3;
         const uint32_t ix = __float_as_uint(kx) & 31u, in_ = __float_as_uint(kn) & 31u;
         const int chx = 16 * (int)(ix >> 2) + 8 * (int)((ix >> 1) & 1) + 2 * qx + (int)(ix & 1);
@@ -777,9 +775,11 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
     // |key - r64| <= 2^-19 |r| + 2^-24 |r| + 2^-23 |m|: window of twice that
     const float tolx = TWO_M17 * Rm + 4.76837158203125e-07f * Mc;
     hib[kk] = gmx[kk] - tolx; lob[kk] = gmn[kk] + tolx;
+    // elements in either window (one predicate per element); equals the two windows' total
+    // count when they are disjoint (hib > lob, required by the fast test below)
     cnt[kk] = 0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) cnt[kk] -= win2(rr[e][kk], hib[kk], lob[kk]);
+    for (int e = 0; e < 16; ++e) win_or(cnt[kk], rr[e][kk], hib[kk], lob[kk]);
     // fp32 params from the keyed extrema, codes from the keys; |y - y_exact| <= inv (4 2^-19 R +
     // 2^-21 (R + M) + 2^-23 span)
     // + qmax 2^-22 + 2^-24, doubled (K1-TC)
@@ -810,7 +810,7 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
     const int ch = 16 * jb + 2 * q + (kk & 1) + 8 * (kk >> 1);
-    const bool fast = cnt[kk] == 2 && __popc(bmx[kk]) == 1 && __popc(bmn[kk]) == 1;
+    const bool fast = cnt[kk] == 2 && hib[kk] > lob[kk] && __popc(bmx[kk]) == 1 && __popc(bmn[kk]) == 1;
     const int gx = (__ffs(bmx[kk]) - 1) >> 2, gn = (__ffs(bmn[kk]) - 1) >> 2;
     const uint32_t ix = __float_as_uint(gmx[kk]) & 15u, in_ = __float_as_uint(gmn[kk]) & 15u;
     const int tx = 16 * (int)(ix >> 1) + 8 * (int)(ix & 1) + gx;
