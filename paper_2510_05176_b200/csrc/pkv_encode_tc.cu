@@ -358,7 +358,9 @@ struct RowStats {
   float kmx[2], kmn[2];   // lane-local keyed extrema of r (5-bit element index)
   float xmx[2], xmn[2];   // lane-local extrema of x
 };
-template <bool STORE>
+// KEYED: extrema of keys (the owner's index in the low bits, V); else plain extrema of r (K
+// tokens need only max - min; the keyed error bound derr covers both)
+template <bool STORE, bool KEYED = true>
 __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* M, int tb, int lane, const int idx[2],
                                            float (&r)[2][8][4], RowStats& st) {
   const int q = lane & 3;
@@ -390,8 +392,10 @@ __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* 
         for (int e = 0; e < 4; ++e) r[h][j][e] = rv[h][e];
       }
       const float* xx = h ? x1 : x0;
-      const float k0 = fkey(rv[h][0], 4 * j + 0, 0xffffffe0u), k1 = fkey(rv[h][1], 4 * j + 1, 0xffffffe0u);
-      const float k2 = fkey(rv[h][2], 4 * j + 2, 0xffffffe0u), k3 = fkey(rv[h][3], 4 * j + 3, 0xffffffe0u);
+      const float k0 = KEYED ? fkey(rv[h][0], 4 * j + 0, 0xffffffe0u) : rv[h][0];
+      const float k1 = KEYED ? fkey(rv[h][1], 4 * j + 1, 0xffffffe0u) : rv[h][1];
+      const float k2 = KEYED ? fkey(rv[h][2], 4 * j + 2, 0xffffffe0u) : rv[h][2];
+      const float k3 = KEYED ? fkey(rv[h][3], 4 * j + 3, 0xffffffe0u) : rv[h][3];
       st.kmx[h] = fmax3(st.kmx[h], k0, k1); st.kmx[h] = fmax3(st.kmx[h], k2, k3);
       st.kmn[h] = fmin3(st.kmn[h], k0, k1); st.kmn[h] = fmin3(st.kmn[h], k2, k3);
       st.xmx[h] = fmax3(st.xmx[h], xx[0], xx[1]); st.xmx[h] = fmax3(st.xmx[h], xx[2], xx[3]);
@@ -498,7 +502,7 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
   const int idx[2] = {i0, i1};
   float r[2][8][4];
   RowStats st;
-  resid_tile<VS>(X, M, tb, lane, idx, r, st);
+  resid_tile<VS, VS>(X, M, tb, lane, idx, r, st);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const float kx = qmax4(st.kmx[h]), kn = qmin4(st.kmn[h]);
