@@ -387,15 +387,14 @@ __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* 
                             {__fsub_rn(x1[0], m1.x), __fsub_rn(x1[1], m1.y), __fsub_rn(x1[2], m1.z), __fsub_rn(x1[3], m1.w)}};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if constexpr (STORE) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) r[h][j][e] = rv[h][e];
-      }
       const float* xx = h ? x1 : x0;
       const float k0 = KEYED ? fkey(rv[h][0], 4 * j + 0, 0xffffffe0u) : rv[h][0];
       const float k1 = KEYED ? fkey(rv[h][1], 4 * j + 1, 0xffffffe0u) : rv[h][1];
       const float k2 = KEYED ? fkey(rv[h][2], 4 * j + 2, 0xffffffe0u) : rv[h][2];
       const float k3 = KEYED ? fkey(rv[h][3], 4 * j + 3, 0xffffffe0u) : rv[h][3];
+      if constexpr (STORE) {  // the keys (or r when not KEYED)
+        r[h][j][0] = k0; r[h][j][1] = k1; r[h][j][2] = k2; r[h][j][3] = k3;
+      }
       st.kmx[h] = fmax3(st.kmx[h], k0, k1); st.kmx[h] = fmax3(st.kmx[h], k2, k3);
       st.kmn[h] = fmin3(st.kmn[h], k0, k1); st.kmn[h] = fmin3(st.kmn[h], k2, k3);
       st.xmx[h] = fmax3(st.xmx[h], xx[0], xx[1]); st.xmx[h] = fmax3(st.xmx[h], xx[2], xx[3]);
@@ -462,7 +461,7 @@ __device__ __noinline__ void cand_stats(const unsigned char* X, const float* M, 
   float r[2][8][4];
   RowStats st;
   const int idx[2] = {p0, p1};
-  resid_tile<false>(X, M, tb, lane, idx, r, st);
+  resid_tile<false, false>(X, M, tb, lane, idx, r, st);  // candidates compare plain distances
   out[0] = st.kmx[0]; out[1] = st.kmn[0]; out[2] = st.kmx[1]; out[3] = st.kmn[1];
 }
 // fp64 extrema of V row t over the elements whose key (fragment-layout index) lies in the
@@ -518,7 +517,7 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          win_or(cnt, fkey(r[h][j][e], 4 * j + e, 0xffffffe0u), hib, lob);
+          win_or(cnt, r[h][j][e], hib, lob);  // r holds the keys
         }
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
