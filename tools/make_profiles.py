@@ -54,9 +54,13 @@ def main():
     traffic = {}
     # token-units (units x committed tokens) of the captured launches (tools/gpu_profiles.sh MED config)
     units = int(os.environ.get("PROF_UNITS", 2 * 32 * 8)) * int(os.environ.get("PROF_COMMITTED", 32768 - 128))
-    for name in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn"):
-        rep = os.path.join(OUT, name + ".ncu-rep")
-        if not os.path.exists(rep):
+    # only reports from this capture: within an hour of the newest one (older reports left in
+    # gpurun_out/ by earlier captures would describe superseded kernels)
+    reps = {n: os.path.join(OUT, n + ".ncu-rep")
+            for n in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn")}
+    newest = max((os.path.getmtime(r) for r in reps.values() if os.path.exists(r)), default=0.0)
+    for name, rep in reps.items():
+        if not os.path.exists(rep) or os.path.getmtime(rep) < newest - 3600:
             continue
         txt = "\n".join(ncu_summary.details(rep))
         raw = ncu_summary.raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
