@@ -698,7 +698,17 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
         b_tile<SIDE == 1>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
       }
     }
-    if (q == 0) { sc.fidx()[t0] = idx[0]; sc.fidx()[t0 + 8] = idx[1]; }
+    if (q == 0) {
+      sc.fidx()[t0] = idx[0]; sc.fidx()[t0 + 8] = idx[1];
+      if constexpr (SIDE == 0) {  // K: the final row's float offsets for even / odd channel chunks
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int pp = idx[h], pl = pp & 1;
+          sc.guess()[t0 + 8 * h] = pp * 128 + 4 * pl;  // mslot: (c ^ pl) = c + pl for even c
+          reinterpret_cast<int*>(sc.cand())[t0 + 8 * h] = pp * 128 - 4 * pl;  // c - pl for odd c
+        }
+      }
+    }
   }
   __syncwarp();
 }
@@ -719,8 +729,8 @@ __device__ __forceinline__ void k_load(const unsigned char* X, const float* M, c
     const unsigned char* rowp = X + hsel + t * 128 + cw;
     const uint32_t xa = *reinterpret_cast<const uint32_t*>(rowp + ((ck ^ (t & 7)) << 4));
     const uint32_t xb = *reinterpret_cast<const uint32_t*>(rowp + (((ck + 1) ^ (t & 7)) << 4));
-    const int p = fi[e];
-    const float4 m = *reinterpret_cast<const float4*>(M + p * 128 + mslot(p, q, jb));
+    // mslot(p, q, jb) = q*32 + 4 ((jb ^ 2q) & 7) + (+-4 (p & 1), folded into fi[e])
+    const float4 m = *reinterpret_cast<const float4*>(M + fi[e] + q * 32 + 4 * ((jb ^ (2 * q)) & 7));
     rr[e][0] = __fsub_rn(h2f_lo(xa), m.x); rr[e][1] = __fsub_rn(h2f_hi(xa), m.y);
     rr[e][2] = __fsub_rn(h2f_lo(xb), m.z); rr[e][3] = __fsub_rn(h2f_hi(xb), m.w);
     if (!FULL && t >= L) rr[e][0] = rr[e][1] = rr[e][2] = rr[e][3] = FE_NAN;
@@ -740,9 +750,11 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
   constexpr int QMAX = (1 << BITS) - 1;
   constexpr int HS = 8 / BITS;
   const int g = lane >> 2, q = lane & 3;
+  // per token: float offset of its pattern row (token stage D), parity-adjusted for this chunk
+  const int* moff = (jb & 1) ? reinterpret_cast<const int*>(sc.cand()) : sc.guess();
   int fi[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) fi[e] = sc.fidx()[16 * (e >> 1) + 8 * (e & 1) + g];
+  for (int e = 0; e < 16; ++e) fi[e] = moff[16 * (e >> 1) + 8 * (e & 1) + g];
   float rr[16][4];
   k_load<FULL>(X, M, fi, jb, g, q, L, rr);
   // keys replace r from here on: the codes below absorb their 2^-19 |r| error in the guard
