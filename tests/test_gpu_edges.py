@@ -1,0 +1,142 @@
+"""Edge cases of the B200 path against the CPU oracle (bit-exact decisions, codes and
+params; attention within 1e-3 of fp64 softmax):
+
+* prefill no longer than the window: nothing committed (engine.py:162-165), attention over
+  the exact window alone, then decode appends up to and past the first flush;
+* a one-token committed span (T = W + 1) on the K1-TC envelope (fp16, d = G = 128);
+* P = 64 patterns, outside K1-TC (P <= 32): the K1 span encoder;
+* far more units than CTAs with one span each (work queue: fewer items per CTA than
+  subgroups), K1-TC against K1.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import pkv_oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def pkv():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_05176_b200 as P
+    return P
+
+
+def _units(n, T, d, seed):
+    ks, vs = [], []
+    for u in range(n):
+        k, v = O.synth_unit(O.unit_seed(seed, 1, u), T, d)
+        ks.append(k.astype(np.float16).astype(np.float64))
+        vs.append(v.astype(np.float16).astype(np.float64))
+    return np.stack(ks), np.stack(vs)
+
+
+def _assert_matches_oracle(cache, heads):
+    from paper_2510_05176_b200.export import export_unit
+
+    for u, h in enumerate(heads):
+        st = export_unit(cache, u, with_bytes=False)
+        np.testing.assert_array_equal(st.kpat, h.kpat)
+        np.testing.assert_array_equal(st.vpat, h.vpat)
+        assert len(st.kb_start) == len(h.k_blocks)
+        if h.k_blocks:
+            np.testing.assert_array_equal(st.k_idx, np.concatenate([b[5] for b in h.k_blocks]))
+            np.testing.assert_array_equal(st.k_codes, np.concatenate([b[4] for b in h.k_blocks]))
+            np.testing.assert_array_equal(st.k_scale, np.stack([b[2] for b in h.k_blocks]))
+            np.testing.assert_array_equal(st.k_zero, np.stack([b[3] for b in h.k_blocks]))
+            np.testing.assert_array_equal(st.v_idx, np.array([t[3] for t in h.v_tok]))
+            np.testing.assert_array_equal(st.v_codes, np.stack([t[2] for t in h.v_tok]))
+            np.testing.assert_array_equal(st.v_scale, np.array([t[0] for t in h.v_tok]))
+            np.testing.assert_array_equal(st.v_zero, np.array([t[1] for t in h.v_tok]))
+        np.testing.assert_array_equal(st.window_k, np.stack(h.win_k))
+        np.testing.assert_array_equal(st.window_v, np.stack(h.win_v))
+
+
+def _attention_close(pkv, cache, U, d, G=4, seed=3):
+    q = np.random.default_rng(seed).normal(size=(U, G, d)).astype(np.float32)
+    out = cache.decode_attention(torch.from_numpy(q).cuda()).cpu().numpy()
+    kc, vc = cache.dequant()
+    wk, wv = cache.window()
+    for u in range(U):
+        kall = np.concatenate([kc[u].cpu().numpy(), wk[u].double().cpu().numpy()])
+        vall = np.concatenate([vc[u].cpu().numpy(), wv[u].double().cpu().numpy()])
+        ref = O.attention(q[u].astype(np.float64), kall, vall, 1.0 / math.sqrt(d))
+        assert np.abs(out[u] - ref).max() <= 1e-3 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("T", [1, 60, 128])
+def test_prefill_within_window_then_first_flush(pkv, T):
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, d = 3, 128
+    S = 256 - T + 5  # past the first flush at len == W + G (engine.py:186)
+    ec = EngineConfig(bits=2, pattern_count=8)
+    k, v = _units(U, T + S, d, seed=T)
+    heads = [O.replay(k[u, :T], v[u, :T], k[u, T:T + S], v[u, T:T + S], O.Knobs(bits=2, pattern_count=8))
+             for u in range(U)]
+    cache = pkv.PatternKVCache(ec, U, d, dtype=torch.float16, max_tokens=T + S + 256)
+    kt, vt = torch.from_numpy(k).half().cuda(), torch.from_numpy(v).half().cuda()
+    cache.prefill(kt[:, :T], vt[:, :T])
+    assert cache.info().committed_count == 0
+    _attention_close(pkv, cache, U, d)
+    for t in range(T, T + S):
+        cache.append(kt[:, t], vt[:, t])
+    assert cache.info().committed_count == heads[0].committed > 0
+    _assert_matches_oracle(cache, heads)
+    _attention_close(pkv, cache, U, d)
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+def test_one_token_span(pkv, bits):
+    """T = W + 1: the prefill commits a single-token span (K groups of one element)."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, d, T = 4, 128, 129
+    ec = EngineConfig(bits=bits, pattern_count=16)
+    k, v = _units(U, T, d, seed=40 + bits)
+    heads = [O.replay(k[u], v[u], k[u, :0], v[u, :0], O.Knobs(bits=bits, pattern_count=16)) for u in range(U)]
+    cache = pkv.PatternKVCache(ec, U, d, dtype=torch.float16, max_tokens=T + 256)
+    cache.prefill(torch.from_numpy(k).half().cuda(), torch.from_numpy(v).half().cuda())
+    assert cache.info().committed_count == 1
+    _assert_matches_oracle(cache, heads)
+
+
+def test_sixty_four_patterns_span_encoder(pkv):
+    """P = 64 (K1-TC serves P <= 32): the K1 span encoder, fp16, against the oracle."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, d, T = 2, 128, 1100
+    ec = EngineConfig(bits=2, pattern_count=64)
+    k, v = _units(U, T, d, seed=64)
+    heads = [O.replay(k[u], v[u], k[u, :0], v[u, :0], O.Knobs(bits=2, pattern_count=64)) for u in range(U)]
+    cache = pkv.PatternKVCache(ec, U, d, dtype=torch.float16, max_tokens=T + 256)
+    cache.prefill(torch.from_numpy(k).half().cuda(), torch.from_numpy(v).half().cuda())
+    _assert_matches_oracle(cache, heads)
+
+
+def test_many_units_one_span_each(pkv, monkeypatch):
+    """600 units x one 128-token span: fewer queue items per CTA than subgroups; K1-TC == K1
+    on the codes and the exact fp64 reconstruction (params, indices, codes)."""
+    from paper_2510_05176_b200.config import EngineConfig
+    from paper_2510_05176_b200.synth import synth_kv
+
+    U, T = 600, 256
+    ec = EngineConfig(bits=2, pattern_count=16)
+    k, v = synth_kv(U, T, 128, seed=5)
+    out = []
+    for tc in ("1", "0"):
+        monkeypatch.setenv("PKV_ENCODE_TC", tc)
+        cache = pkv.PatternKVCache(ec, U, 128, dtype=torch.float16, max_tokens=T + 256)
+        cache.prefill(k, v)
+        kc, vc = cache.codes()
+        kd, vd = cache.dequant()
+        out.append((kc.cpu(), vc.cpu(), kd.cpu(), vd.cpu()))
+        del cache
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
