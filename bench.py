@@ -54,6 +54,23 @@ def ncu_traffic(kernel: str, token_units: int):
         return None
 
 
+def issue_ceiling(kernel: str, bytes_per_token_unit: float, sm_mhz):
+    """Instruction-issue ceiling of `kernel` (report encode against min(HBM, ALU)):
+    warp-instructions per token-unit from the committed ncu capture (profiles/traffic.json),
+    4 issues/clock on each SM at the clock measured during the timed region."""
+    import torch
+
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            ipt = float(json.load(f)["warp_instr_per_token_unit"][kernel])
+        nsm = torch.cuda.get_device_properties(0).multi_processor_count
+        hz = float(sm_mhz) * 1e6
+    except Exception:
+        return None
+    return {"warp_instr_per_token_unit": ipt, "sm_mhz": sm_mhz,
+            "ceiling_GBps": nsm * 4 * hz / ipt * bytes_per_token_unit / 1e9}
+
+
 def enc_bytes_per_token(bits: int, d: int = 128, g: int = 128) -> int:
     """Algorithmic HBM bytes per encoded token-unit (this build's layout):
     read fp16 K+V (4d) ; write K codes + V codes (2*b*d/8), K params f32+f64
@@ -357,6 +374,10 @@ def main():
         return
 
     r = results[args.bits]
+    # instruction-issue ceiling of the encode kernel (the committed capture is the 2-bit kernel)
+    enc_ceiling = issue_ceiling("encode", r["bpt"], (r["clk"] or {}).get("sm_mhz")) if args.bits == 2 else None
+    if enc_ceiling:
+        enc_ceiling["frac"] = (r["enc_bytes"] / (r["kern_ms"] * 1e-3) / 1e9) / enc_ceiling["ceiling_GBps"]
     # ---- CPU baseline: oracle port on this host's cores, bounded sample --------------
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -392,7 +413,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": kern_gbps, "peak": peak, "unit": "GB/s",
                      "frac": kern_gbps / peak, "traffic": ncu_traffic("encode", U * committed), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": r["enc_bytes"],
-                     "kernel": f"encode_tc_kernel<{args.bits}> (K1-TC)", "bytes_per_token_unit": r["bpt"]},
+                     "kernel": f"encode_tc_kernel<{args.bits}> (K1-TC)", "bytes_per_token_unit": r["bpt"],
+                     "issue_ceiling": enc_ceiling},
         "decode_attn": {"tokens_per_s": r["tok_s"], "ms_per_step": r["att_ms"], "GBps": r["att_gbps"],
                         "frac": r["att_gbps"] / peak, "bytes_per_step": r["att_bytes"], "gqa": args.gqa,
                         "context": T, "e2e_ms_per_step": results.get("e2e_attn_ms"),

@@ -52,6 +52,7 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "round1"
     os.makedirs(PROF, exist_ok=True)
     traffic = {}
+    instr = {}
     # token-units (units x committed tokens) of the captured launches (tools/gpu_profiles.sh MED config)
     units = int(os.environ.get("PROF_UNITS", 2 * 32 * 8)) * int(os.environ.get("PROF_COMMITTED", 32768 - 128))
     # only reports from this capture: within an hour of the newest one (older reports left in
@@ -65,7 +66,7 @@ def main():
         txt = "\n".join(ncu_summary.details(rep))
         raw = ncu_summary.raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
                                     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-                                    "gpu__time_duration.sum", "launch__grid_size"])
+                                    "gpu__time_duration.sum", "launch__grid_size", "smsp__inst_executed.sum"])
         txt += "\n" + "\n".join(f"{k:60s} {v[0]} {v[1]}" for k, v in raw.items())
         txt += "\n\n" + "\n".join(ncu_summary.sass(rep, nwin=0))
         txt += "\n\nhot source lines (share of executed instructions / of stall samples):\n" + lines(rep)
@@ -77,11 +78,15 @@ def main():
                 return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
             traffic[name.replace("prof_", "").replace("_full", "")] = (
                 to_bytes(raw["dram__bytes_read.sum"]) + to_bytes(raw["dram__bytes_write.sum"])) / units
+            if "smsp__inst_executed.sum" in raw:
+                instr[name.replace("prof_", "").replace("_full", "")] = (
+                    float(raw["smsp__inst_executed.sum"][0].replace(",", "")) / units)
     if traffic:
         with open(os.path.join(PROF, "traffic.json"), "w") as f:
             json.dump({"source": f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum ({tag}), "
                                  f"per token-unit of the captured launch ({units} token-units)",
-                       "bytes_per_token_unit": traffic}, f, indent=1)
+                       "bytes_per_token_unit": traffic,
+                       "warp_instr_per_token_unit": instr}, f, indent=1)
     lp = os.path.join(OUT, "launches.csv")
     if os.path.exists(lp):
         with open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w") as f:
