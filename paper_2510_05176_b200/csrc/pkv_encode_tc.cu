@@ -600,19 +600,27 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
       // |r32 - r64| <= 2^-23 (|x| + |m|) per probe residual, + 2^-24 relative on the range:
       // inside the 2^-21 (|x|max + |m|max) slack
       const float pb = __fadd_rn(dhi, 4.76837158203125e-07f * (xa + pmx));
+      // the first 4 probes prune almost every (token, pattern); the rest are evaluated only
+      // when a lane of the warp still keeps the pattern
 #pragma unroll 4
       for (int p = 0; p < 32; ++p) {
-        float hi = -FE_INF, lo = FE_INF;
+        const float4 m4 = *reinterpret_cast<const float4*>(pt.pm4() + NPRB * p);
+        const float r0 = __fsub_rn(x4[0], m4.x), r1 = __fsub_rn(x4[1], m4.y);
+        const float r2 = __fsub_rn(x4[2], m4.z), r3 = __fsub_rn(x4[3], m4.w);
+        float hi = fmaxf(fmax3(r0, r1, r2), r3), lo = fminf(fmin3(r0, r1, r2), r3);
+        bool keep = __fsub_rn(hi, lo) <= pb && p < P;
+        if (__any_sync(0xffffffffu, keep)) {
 #pragma unroll
-        for (int j = 0; j < NPRB; j += 4) {
-          const float4 m4 = *reinterpret_cast<const float4*>(pt.pm4() + NPRB * p + j);
-          const float r0 = __fsub_rn(x4[j], m4.x), r1 = __fsub_rn(x4[j + 1], m4.y);
-          const float r2 = __fsub_rn(x4[j + 2], m4.z), r3 = __fsub_rn(x4[j + 3], m4.w);
-          hi = fmaxf(hi, fmax3(r0, r1, r2)); hi = fmaxf(hi, r3);
-          lo = fminf(lo, fmin3(r0, r1, r2)); lo = fminf(lo, r3);
+          for (int j = 4; j < NPRB; j += 4) {
+            const float4 n4 = *reinterpret_cast<const float4*>(pt.pm4() + NPRB * p + j);
+            const float s0 = __fsub_rn(x4[j], n4.x), s1 = __fsub_rn(x4[j + 1], n4.y);
+            const float s2 = __fsub_rn(x4[j + 2], n4.z), s3 = __fsub_rn(x4[j + 3], n4.w);
+            hi = fmaxf(hi, fmax3(s0, s1, s2)); hi = fmaxf(hi, s3);
+            lo = fminf(lo, fmin3(s0, s1, s2)); lo = fminf(lo, s3);
+          }
+          keep = keep && __fsub_rn(hi, lo) <= pb;
         }
-        const float rng = __fsub_rn(hi, lo);
-        mask |= (uint32_t)(rng <= pb && p < P) << p;
+        mask |= (uint32_t)keep << p;
       }
     } else {
       const float dlo = fmaxf(__fsub_rn(dg, T2), 0.f) * 0.9999998f;
