@@ -95,8 +95,6 @@ __device__ __forceinline__ void load_words(const uint8_t* tile, int lane, uint32
   }
 }
 
-constexpr int ATT_STAGES = 4;
-
 // per-lane private pattern-weight copies while they fit in 64 KB
 __host__ __device__ inline bool attn_w_private(int Pv, int NT) {
   return (size_t)ATT_WARPS * 8 * (Pv > 1 ? Pv : 1) * 4 * NT * 4 <= 64 * 1024;

@@ -46,7 +46,6 @@ constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23
 #define FE_INF __int_as_float(0x7f800000)
 #define FE_NAN __int_as_float(0x7fc00000)
 constexpr float TWO_M13 = 1.220703125e-04f;
-constexpr float TWO_M15 = 3.0517578125e-05f;
 constexpr float TWO_M17 = 7.62939453125e-06f;
 constexpr float TWO_M22 = 2.384185791015625e-07f;
 
@@ -69,7 +68,7 @@ constexpr int SZ_SC = NSC * 128 * 4;
 constexpr int OFF_SC = OFF_M + 2 * SZ_M;          // SC[sgi]
 constexpr int NPRB = 8;    // K probe channels of the pruning bound
 constexpr int NFLAG = (2 + NPRB + 3) / 4 * 4;      // P, no-L2, probe channels
-constexpr int SZ_PAT = (4 * 32 + 128 + NFLAG + NPRB * 32) * 4;  // bb, mn, pm, mabsr [4][32], mabsc[128], flags, pm4[32][NPRB]
+constexpr int SZ_PAT = (4 * 32 + 128 + NFLAG + NPRB * 32) * 4;  // bb, mn, (spare), mabsr [4][32], mabsc[128], flags, pm4[32][NPRB]
 constexpr int OFF_PAT = OFF_SC + 4 * SZ_SC;       // PAT[side]
 constexpr int OFF_BAR = OFF_PAT + 2 * SZ_PAT;     // xfull[4], mma[4], release counters[4], tmem addr,
                                                   // chunk ring[2] at +96
@@ -104,7 +103,6 @@ struct Pat {   // per-side pattern scalars
   __device__ explicit Pat(unsigned char* sb, int side) : base(sb + OFF_PAT + side * SZ_PAT) {}
   __device__ float* bb() const { return reinterpret_cast<float*>(base); }            // ||m'_p||^2 (+inf past P)
   __device__ float* mn() const { return reinterpret_cast<float*>(base + 128); }      // ||m'_p||
-  __device__ float* pm() const { return reinterpret_cast<float*>(base + 256); }      // (unused)
   __device__ float* pm4() const { return reinterpret_cast<float*>(base + 1024 + 4 * NFLAG); }  // K: m32 at the probe channels
   __device__ float* mabsr() const { return reinterpret_cast<float*>(base + 384); }   // max_c |m_pc|
   __device__ float* mabsc() const { return reinterpret_cast<float*>(base + 512); }   // max_p |m_pc| (K)
@@ -138,6 +136,7 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a
 __device__ __forceinline__ void warp_converged() {
   uint32_t d;
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(0u));
+  asm volatile("" ::"r"(d));  // consumed (the instruction is what matters)
 }
 __device__ __forceinline__ uint32_t movm_t(uint32_t a) {
   uint32_t d;
