@@ -135,8 +135,7 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a
 // follow in an out-of-line function need no divergence-tolerant (WARPSYNC.COLLECTIVE) copies
 __device__ __forceinline__ void warp_converged() {
   uint32_t d;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(0u));
-  asm volatile("" ::"r"(d));  // consumed (the instruction is what matters)
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(0u));  // result unused
 }
 __device__ __forceinline__ uint32_t movm_t(uint32_t a) {
   uint32_t d;
