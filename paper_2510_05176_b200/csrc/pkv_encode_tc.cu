@@ -1367,8 +1367,8 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
   static int chunk = 0;
   if (!chunk) {
     const char* ce = getenv("PKV_TC_CHUNK");
-    chunk = ce ? atoi(ce) : 16;
-    if (chunk < 4 || chunk > 4096) chunk = 16;
+    chunk = ce ? atoi(ce) : 32;
+    if (chunk < 4 || chunk > 4096) chunk = 32;
   }
   a.k_tpc = (int)(kfrac * (nsm / 2) + 0.5);
   a.chunk = chunk;
