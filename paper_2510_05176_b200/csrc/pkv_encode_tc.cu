@@ -118,9 +118,9 @@ struct Args {
   int64_t nitems;        // U * nb
   double yq;             // RN(1 / qmax)
   int k_tpc;             // TPCs [0, k_tpc) start on K, the rest on V
-  int chunk;             // items per chunk
-  int cpu;               // chunks per unit
-  int nchunks;           // U * cpu per side
+  int chunk[2];          // items per chunk (K, V)
+  int cpu[2];            // chunks per unit
+  int nchunks[2];        // U * cpu
 };
 
 __device__ __forceinline__ void bar_side() { asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory"); }
@@ -1113,10 +1113,10 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
   int* ring = reinterpret_cast<int*>(sb + OFF_BAR + 96);
   auto chunk_items = [&](int ch, int64_t& b0, int64_t& b1) {
     b0 = b1 = 0;
-    if (ch >= A.nchunks) return;
-    const int uu = ch / A.cpu, pc = ch % A.cpu;
-    b0 = (int64_t)uu * nb + pc * A.chunk;
-    b1 = (int64_t)uu * nb + min(nb, (pc + 1) * A.chunk);
+    if (ch >= A.nchunks[SIDE]) return;
+    const int uu = ch / A.cpu[SIDE], pc = ch % A.cpu[SIDE];
+    b0 = (int64_t)uu * nb + pc * A.chunk[SIDE];
+    b1 = (int64_t)uu * nb + min(nb, (pc + 1) * A.chunk[SIDE]);
   };
   const int64_t row0 = c.blk_start[A.first_block];
   auto issue = [&](int64_t item) {
@@ -1132,11 +1132,11 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
   int64_t pending = -1;  // item whose TMA this subgroup already issued
   for (;;) {
     const int cur = ring[0], nx = ring[1];
-    if (cur >= A.nchunks) break;
+    if (cur >= A.nchunks[SIDE]) break;
     int64_t i0, i1, j0, j1;
     chunk_items(cur, i0, i1);
     chunk_items(nx, j0, j1);
-    const int u = cur / A.cpu;
+    const int u = cur / A.cpu[SIDE];
     if (u != staged) {
       stage_patterns(A, SIDE, u, sb, gtid);
       bar_side();
@@ -1364,18 +1364,24 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
     kfrac = kf ? atof(kf) : 1.0;
     if (!(kfrac > 0.0 && kfrac <= 1.0)) kfrac = 1.0;
   }
-  static int chunk = 0;
+  static int chunk = 0, chunk_v = 0;
   if (!chunk) {
     const char* ce = getenv("PKV_TC_CHUNK");
     chunk = ce ? atoi(ce) : 32;
     if (chunk < 4 || chunk > 4096) chunk = 32;
+    const char* cv = getenv("PKV_TC_CHUNK_V");
+    chunk_v = cv ? atoi(cv) : chunk;
+    if (chunk_v < 4 || chunk_v > 4096) chunk_v = chunk;
   }
   a.k_tpc = (int)(kfrac * (nsm / 2) + 0.5);
-  a.chunk = chunk;
-  a.cpu = (nblocks + chunk - 1) / chunk;
-  if ((int64_t)c.U * a.cpu + 2 * nsm >= (1ll << 31)) return cudaErrorNotSupported;
-  a.nchunks = c.U * a.cpu;
-  const int grid = (int)std::min<int64_t>(nsm, 2 * (int64_t)a.nchunks);
+  a.chunk[0] = chunk;
+  a.chunk[1] = chunk_v;
+  for (int sd = 0; sd < 2; ++sd) {
+    a.cpu[sd] = (nblocks + a.chunk[sd] - 1) / a.chunk[sd];
+    if ((int64_t)c.U * a.cpu[sd] + 2 * nsm >= (1ll << 31)) return cudaErrorNotSupported;
+    a.nchunks[sd] = c.U * a.cpu[sd];
+  }
+  const int grid = (int)std::min<int64_t>(nsm, (int64_t)a.nchunks[0] + a.nchunks[1]);
   if (cudaMemsetAsync(c.work, 0, 16, st) != cudaSuccess) return cudaGetLastError();
   if (c.bits == 2) {
     cudaFuncSetAttribute(fe::encode_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::smem_bytes(2));
