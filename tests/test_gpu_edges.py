@@ -6,7 +6,8 @@ params; attention within 1e-3 of fp64 softmax):
 * a one-token committed span (T = W + 1) on the K1-TC envelope (fp16, d = G = 128);
 * P = 64 patterns, outside K1-TC (P <= 32): the K1 span encoder;
 * far more units than CTAs with one span each (work queue: fewer items per CTA than
-  subgroups), K1-TC against K1.
+  subgroups), K1-TC against K1;
+* bf16 and fp32 inputs through prefill and decode flushes.
 """
 import math
 
@@ -140,3 +141,29 @@ def test_many_units_one_span_each(pkv, monkeypatch):
         del cache
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("tdt", [torch.bfloat16, torch.float32])
+def test_bf16_fp32_inputs_prefill_decode(pkv, tdt):
+    """bf16 / fp32 caches (the K1 span encoder; K1-TC is fp16-only): prefill + decode flushes
+    bit-exact vs the oracle on the same (rounded) inputs, attention within 1e-3."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, d, T, S = 3, 128, 700, 150
+    ec = EngineConfig(bits=4, pattern_count=16)
+    ks, vs = [], []
+    for u in range(U):
+        k, v = O.synth_unit(O.unit_seed(77, 2, u), T + S, d)
+        ks.append(torch.from_numpy(k).to(tdt))
+        vs.append(torch.from_numpy(v).to(tdt))
+    kt, vt = torch.stack(ks), torch.stack(vs)
+    k64, v64 = kt.double().numpy(), vt.double().numpy()
+    heads = [O.replay(k64[u, :T], v64[u, :T], k64[u, T:], v64[u, T:], O.Knobs(bits=4, pattern_count=16))
+             for u in range(U)]
+    cache = pkv.PatternKVCache(ec, U, d, dtype=tdt, max_tokens=T + S + 256)
+    kt, vt = kt.cuda(), vt.cuda()
+    cache.prefill(kt[:, :T], vt[:, :T])
+    for t in range(T, T + S):
+        cache.append(kt[:, t], vt[:, t])
+    _assert_matches_oracle(cache, heads)
+    _attention_close(pkv, cache, U, d)
