@@ -7,7 +7,8 @@ params; attention within 1e-3 of fp64 softmax):
 * P = 64 patterns, outside K1-TC (P <= 32): the K1 span encoder;
 * far more units than CTAs with one span each (work queue: fewer items per CTA than
   subgroups), K1-TC against K1;
-* bf16 and fp32 inputs through prefill and decode flushes.
+* bf16 and fp32 inputs through prefill and decode flushes;
+* head_dim 64 / 96 / 40 (the KT = 4 attention kernel, padded channels).
 """
 import math
 
@@ -167,3 +168,23 @@ def test_bf16_fp32_inputs_prefill_decode(pkv, tdt):
         cache.append(kt[:, t], vt[:, t])
     _assert_matches_oracle(cache, heads)
     _attention_close(pkv, cache, U, d)
+
+
+@pytest.mark.parametrize("d,bits,gqa", [(64, 2, 4), (96, 4, 8), (40, 2, 2)])
+def test_small_head_dims(pkv, d, bits, gqa):
+    """head_dim < 128: Dp = 64 (the KT = 4 attention kernel) or padded channels (96 -> 128,
+    40 -> 64); fp16 caches off the K1-TC envelope, bit-exact vs the oracle, attention 1e-3."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, T, S = 2, 600, 140
+    ec = EngineConfig(bits=bits, pattern_count=12)
+    k, v = _units(U, T + S, d, seed=d)
+    heads = [O.replay(k[u, :T], v[u, :T], k[u, T:], v[u, T:], O.Knobs(bits=bits, pattern_count=12))
+             for u in range(U)]
+    cache = pkv.PatternKVCache(ec, U, d, dtype=torch.float16, max_tokens=T + S + 256)
+    kt, vt = torch.from_numpy(k).half().cuda(), torch.from_numpy(v).half().cuda()
+    cache.prefill(kt[:, :T], vt[:, :T])
+    for t in range(T, T + S):
+        cache.append(kt[:, t], vt[:, t])
+    _assert_matches_oracle(cache, heads)
+    _attention_close(pkv, cache, U, d, G=gqa)
