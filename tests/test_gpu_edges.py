@@ -8,7 +8,8 @@ params; attention within 1e-3 of fp64 softmax):
 * far more units than CTAs with one span each (work queue: fewer items per CTA than
   subgroups), K1-TC against K1;
 * bf16 and fp32 inputs through prefill and decode flushes;
-* head_dim 64 / 96 / 40 (the KT = 4 attention kernel, padded channels).
+* head_dim 64 / 96 / 40 (the KT = 4 attention kernel, padded channels);
+* cfg3's 131072-token context.
 """
 import math
 
@@ -188,3 +189,35 @@ def test_small_head_dims(pkv, d, bits, gqa):
         cache.append(kt[:, t], vt[:, t])
     _assert_matches_oracle(cache, heads)
     _attention_close(pkv, cache, U, d, G=gqa)
+
+
+def test_long_context_cfg3_length(pkv, monkeypatch):
+    """cfg3's 131072-token context (1023 spans per unit): K1-TC == K1 on codes and the exact fp64
+    reconstruction, and attention within 1e-3 of fp64 softmax over it (torch fp64 on the device;
+    the numpy oracle is too slow at this length)."""
+    from paper_2510_05176_b200.config import EngineConfig
+    from paper_2510_05176_b200.synth import synth_kv
+
+    U, T, d, G = 2, 131072, 128, 4
+    ec = EngineConfig(bits=2, pattern_count=32)
+    k, v = synth_kv(U, T, d, seed=131)
+    res = []
+    for tc in ("1", "0"):
+        monkeypatch.setenv("PKV_ENCODE_TC", tc)
+        cache = pkv.PatternKVCache(ec, U, d, dtype=torch.float16, max_tokens=T + 256)
+        cache.prefill(k, v)
+        kc, vc = cache.codes()
+        kd, vd = cache.dequant()
+        res.append((kc, vc, kd, vd))
+        if tc == "1":
+            q = torch.randn((U, G, d), device="cuda", dtype=torch.float32)
+            out = cache.decode_attention(q).double()
+            wk, wv = cache.window()
+            for u in range(U):
+                kall = torch.cat([kd[u], wk[u].double()])
+                vall = torch.cat([vd[u], wv[u].double()])
+                ref = torch.softmax(q[u].double() @ kall.T / math.sqrt(d), dim=-1) @ vall
+                assert (out[u] - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+        del cache
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)
