@@ -509,83 +509,82 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
         }
         __syncthreads();
       }
-      // ---- stable per-cluster point lists (index order) ------------------------
-      if (tid == 0) {
-        int s = 0;
-        for (int j = 0; j < k; ++j) { sm.off[j] = s; s += sm.cnt[j]; }
-      }
-      __syncthreads();
-      for (int64_t base = 0; base < Tn; base += MINE_THREADS) {
-        const int64_t t = base + tid;
-        const int l = t < Tn ? lab[t] : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, l);
-        const int rank_w = __popc(peers & ((1u << lane) - 1));
-        for (int i = tid; i < 16 * k; i += MINE_THREADS) sm.wcnt[i] = 0;
-        __syncthreads();
-        if (l >= 0 && rank_w == 0) sm.wcnt[warp * k + l] = __popc(peers);
-        __syncthreads();
-        if (l >= 0) {
-          int pre = 0;
-          for (int w = 0; w < warp; ++w) pre += sm.wcnt[w * k + l];
-          list[sm.off[l] + pre + rank_w] = (int)t;
-        }
-        __syncthreads();
-        for (int j = tid; j < k; j += MINE_THREADS) {
-          int tot = 0;
-          for (int w = 0; w < 16; ++w) tot += sm.wcnt[w * k + j];
-          sm.off[j] += tot;
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        int s = 0;
-        for (int j = 0; j < k; ++j) { sm.off[j] = s; s += sm.cnt[j]; }
-      }
-      __syncthreads();
       // ---- centers = sequential fp64 means (numpy axis-0 reduction order) -------
-      // chains (cluster j, channel cc) summed strictly in point order; 8 chains per
-      // thread advance together so their list/X loads are in flight concurrently.
-      // The objective of this round (patterns.py:121) is a second pass over the
-      // same chains against the new means.
-      double part = 0.0;
-      for (int i0 = tid; i0 < k * D; i0 += 8 * MINE_THREADS) {
-        const int* lp[8];
-        int nn[8], ch[8], jj[8];
-        double acc[8];
-        int nmax = 0;
+      // Points stream in index order, one thread per channel: every (cluster, channel) chain
+      // receives its members' values in point order, exactly the additions of a per-cluster
+      // walk; the running sum of the current label run stays in a register, and a chain's
+      // first member is assigned (numpy starts the reduction from the first row, so a lone
+      // -0.0 stays -0.0).  Coalesced row loads, no member lists.
+      for (int c0 = 0; c0 < D; c0 += MINE_THREADS) {
+        const int c = c0 + tid;
+        const bool act = c < D;  // warp-uniform for D % 32 == 0; inactive lanes still shuffle
+        uint32_t started[(KMAX + 31) / 32];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int i = i0 + e * MINE_THREADS;
-          const bool ok = i < k * D;
-          jj[e] = ok ? i / D : 0;
-          ch[e] = ok ? i - jj[e] * D : 0;
-          nn[e] = ok ? sm.cnt[jj[e]] : 0;
-          lp[e] = list + sm.off[jj[e]];
-          acc[e] = nn[e] > 0 ? to_f64(X[(int64_t)lp[e][0] * D + ch[e]]) : 0.0;
-          nmax = max(nmax, nn[e]);
-        }
-        for (int q = 1; q < nmax; ++q) {
-          double xv[8];
+        for (int w = 0; w < (KMAX + 31) / 32; ++w) started[w] = 0u;
+        int curj = -1;
+        double racc = 0.0;
+        // 16-point blocks: lane e holds the label of point tb + e (one coalesced load); the
+        // next block's labels and values load while this block's additions run
+        constexpr int PB = 16;
+        int myl = lane < PB && lane < Tn ? lab[lane] : -1;
+        T xv[PB];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) xv[e] = q < nn[e] ? to_f64(X[(int64_t)lp[e][q] * D + ch[e]]) : 0.0;
+        for (int e = 0; e < PB; ++e) xv[e] = (act && e < Tn) ? X[(int64_t)e * D + c] : T(0);
+        for (int64_t tb = 0; tb < Tn; tb += PB) {
+          const int64_t tn = tb + PB;
+          const int nl = (lane < PB && tn + lane < Tn) ? lab[tn + lane] : -1;
+          T nx[PB];
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (q < nn[e]) acc[e] = __dadd_rn(acc[e], xv[e]);
-        }
-        double mean[8];
+          for (int e = 0; e < PB; ++e) nx[e] = (act && tn + e < Tn) ? X[(tn + e) * D + c] : T(0);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          mean[e] = nn[e] > 0 ? __ddiv_rn(acc[e], (double)nn[e]) : 0.0;
-          if (nn[e] > 0) sm.cen[jj[e] * sm.CST + ch[e]] = mean[e];
-        }
-        for (int q = 0; q < nmax; ++q) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            if (q < nn[e]) {
-              const double d = __dsub_rn(to_f64(X[(int64_t)lp[e][q] * D + ch[e]]), mean[e]);
-              part = fma(d, d, part);
+          for (int e = 0; e < PB; ++e) {
+            const int jt = __shfl_sync(0xffffffffu, myl, e);
+            if (jt < 0) break;  // past Tn (uniform)
+            const double x = to_f64(xv[e]);
+            if (jt == curj) {
+              racc = __dadd_rn(racc, x);
+            } else {
+              if (curj >= 0 && act) sm.cen[curj * sm.CST + c] = racc;
+              const uint32_t bit = 1u << (jt & 31);
+              racc = ((started[jt >> 5] & bit) && act) ? __dadd_rn(sm.cen[jt * sm.CST + c], x) : x;
+              started[jt >> 5] |= bit;
+              curj = jt;
             }
           }
+          myl = nl;
+#pragma unroll
+          for (int e = 0; e < PB; ++e) xv[e] = nx[e];
+        }
+        if (act) {
+          if (curj >= 0) sm.cen[curj * sm.CST + c] = racc;
+          for (int jj = 0; jj < k; ++jj)
+            if ((started[jj >> 5] >> (jj & 31)) & 1)
+              sm.cen[jj * sm.CST + c] = __ddiv_rn(sm.cen[jj * sm.CST + c], (double)sm.cnt[jj]);
+        }
+      }
+      __syncthreads();
+      // The objective of this round (patterns.py:121) against the new means: any order
+      // (compared at 1e-12); thread = (channel, quarter of the points), four partial sums.
+      double part = 0.0;
+      {
+        constexpr int NQ = MINE_THREADS / 64;  // >= 1
+        for (int w0 = tid; w0 < D * NQ; w0 += MINE_THREADS) {
+          const int c = w0 % D, qq = w0 / D;
+          const int64_t t0 = Tn * qq / NQ, t1 = Tn * (qq + 1) / NQ;
+          double p4[4] = {0.0, 0.0, 0.0, 0.0};
+          int64_t t = t0;
+          for (; t + 4 <= t1; t += 4) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const double d = __dsub_rn(to_f64(X[(t + e) * D + c]), sm.cen[lab[t + e] * sm.CST + c]);
+              p4[e] = fma(d, d, p4[e]);
+            }
+          }
+          for (; t < t1; ++t) {
+            const double d = __dsub_rn(to_f64(X[t * D + c]), sm.cen[lab[t] * sm.CST + c]);
+            p4[0] = fma(d, d, p4[0]);
+          }
+          part += (p4[0] + p4[1]) + (p4[2] + p4[3]);
         }
       }
       __syncthreads();
