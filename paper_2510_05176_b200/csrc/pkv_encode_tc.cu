@@ -6,27 +6,29 @@
 // and bit-identical outputs, re-organised so that almost every instruction
 // touches data in registers:
 //
-//  * one persistent CTA per SM, 16 warps: warps 0-7 run the K pipeline and
-//    warps 8-15 the V pipeline over the same (unit, span) work items, each with
-//    its own TMA stream (cp.async.bulk.tensor.3d, 128-byte swizzle) of 32 KB
-//    span tiles, so one side's loads and latencies hide under the other's math;
-//  * nearest pattern: one tcgen05.mma chain per span-side computes x . m'_p
-//    (m' = channel-centered pattern split hi + lo in fp16, fp32 accumulator in
-//    TMEM).  The L2-nearest pattern is the guess g; the exact fp32 d_mm to g
-//    comes out of the residual pass; every other pattern is pruned by two exact
-//    lower bounds on d_mm -- Popoviciu (osc(v)^2 >= 4 Var(v), Var from the GEMM)
-//    and a two-channel probe |v_a - v_b| <= osc(v) -- with rigorous fp error
-//    margins.  Survivors (rare) get the full fp32 distance, near ties the
-//    reference's fp64 argmin (lowest index on ties);
-//  * residuals, extrema and codes in mma-fragment register layout (ldmatrix from
-//    the swizzled tile); per-token (V) reductions need 2 shuffles; K's
-//    per-channel groups run on a residual tile in a transposed warp layout; V
-//    codes move to the V^T fragment layout with movmatrix;
-//  * exact fp64 group extrema from fp32 "keys" (value with the element index in
-//    the low mantissa bits) plus a count of the elements inside the fp32 error
-//    window; codes by a magic-number round z = fma(v - lo, 1/s, 1.5*2^23) whose
-//    distance to the rounding boundary is checked per element pair (fp64
-//    recompute of the reference sequence inside the guard band).
+//  * one persistent CTA per SM, 16 warps in four 4-warp subgroups, all on ONE side (K or V)
+//    at a time: chunks of 32 (unit, span) items come from per-side global queues, every CTA
+//    starts on K and moves to V as K drains (a K phase, then a V phase: one code path per SM,
+//    so the hot code stays in the instruction caches); each subgroup streams its own 32 KB
+//    span tiles (cp.async.bulk.tensor.3d, 128-byte swizzle), the last warp out of a tile
+//    issuing the next item's TMA;
+//  * nearest pattern: one tcgen05.mma chain per span computes x . m'_p (m' = channel-centered
+//    pattern split hi + lo in fp16, fp32 accumulator in TMEM).  The L2-nearest pattern is the
+//    guess g; the exact fp32 d_mm to g comes out of the residual pass; every other pattern is
+//    pruned by an exact lower bound on d_mm with rigorous fp error margins -- V: Popoviciu
+//    (osc(v)^2 >= 4 Var(v), Var from the GEMM); K: the residual range over the 8 widest-
+//    spread channels (4 first, the other 4 only for survivors).  Survivors (rare) get the full
+//    fp32 distance, near ties the reference's fp64 argmin (lowest index on ties);
+//  * residuals, extrema and codes in mma-fragment register layout (ldmatrix from the
+//    swizzled tile); per-token (V) reductions need 2 shuffles; K's per-channel groups run on
+//    a residual tile in a transposed warp layout; V codes move to the V^T fragment layout
+//    with movmatrix;
+//  * exact fp64 group extrema from fp32 "keys" (value with the element index in the low
+//    mantissa bits) plus a one-predicate count of the elements inside the fp32 error windows;
+//    codes by a magic-number round z = fma(v - lo, 1/s, 1.5*2^23) whose distance to the
+//    rounding boundary is checked per element pair (fp64 recompute of the reference sequence
+//    inside the guard band).  DESIGN.md section 3 (K1-TC) has the error bounds and the
+//    measurements behind each choice.
 #include <cuda.h>
 
 #include <cstdlib>
