@@ -104,9 +104,11 @@ int pkv_check_finite(const void* x, int32_t dtype, int64_t n, int64_t* first_bad
 /* mine_patterns (patterns.py:145-158) for every unit of one side (0 = K, 1 = V).
  * x: device [U][T][D] of the cache dtype; first_idx: host [U] = first seed index
  * np.random.default_rng(seed).integers(T) (patterns.py:103,135).  history/niter
- * (optional, host) receive the objective history [U][25] and its length [U]. */
+ * (optional, host) receive the objective history [U][25] and its length [U];
+ * labels (optional, device int32 [U][T]) the final assignment (lloyd_kmeans's
+ * second return value, patterns.py:84-85). */
 int pkv_mine(pkv_cache* c, int32_t side, const void* x, int64_t T, const int64_t* first_idx,
-             double* history, int32_t* niter, void* stream);
+             double* history, int32_t* niter, int32_t* labels, void* stream);
 /* install pattern tables (device [U][P][D] fp64) for one side */
 int pkv_set_patterns(pkv_cache* c, int32_t side, const double* pat, int32_t P, void* stream);
 

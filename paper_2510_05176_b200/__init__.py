@@ -10,7 +10,14 @@ __init__.py:10-94) with the reference's signatures, argument meaning and
 error behaviour, executed on the GPU.
 """
 
-from . import _lib  # noqa: F401  (fails loudly when libpkv_b200.so is missing)
+import sys as _sys
+
+from . import _lib
+
+# fail loudly when libpkv_b200.so is missing -- except while `python -m
+# paper_2510_05176_b200.build` is building it from a clean tree
+if not any(a.endswith("paper_2510_05176_b200.build") for a in getattr(_sys, "orig_argv", ())):
+    _lib.load()
 from .analysis import KvStream, bits_per_token, fp16_reference_bits_per_token
 from .cache import PatternKVCache, first_seed_index
 from .config import EngineConfig

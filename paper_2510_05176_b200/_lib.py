@@ -1,8 +1,10 @@
 """ctypes binding of libpkv_b200.so (include/pkv.h).
 
-The library is the product: there is no CPU fallback.  Importing this module
-fails loudly when the shared library is missing; every compute entry point
-fails with UsageError when no CUDA device is present.
+The library is the product: there is no CPU fallback.  Importing the package
+fails loudly when the shared library is missing (``load()``, called by the
+package ``__init__``; only ``python -m paper_2510_05176_b200.build`` skips it so
+a clean tree can build); every compute entry point fails with UsageError when
+no CUDA device is present.
 """
 
 from __future__ import annotations
@@ -15,13 +17,7 @@ from .errors import DataError, UsageError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PKV_LIB") or os.path.join(_HERE, "libpkv_b200.so")  # PKV_LIB: A/B builds only
 
-if not os.path.exists(LIB_PATH):
-    raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2510_05176_b200.build` "
-        "(the B200 codec has no CPU fallback)"
-    )
-
-lib = C.CDLL(LIB_PATH)
+lib = None  # the loaded CDLL (load())
 
 PKV_OK, PKV_USAGE, PKV_DATA, PKV_CUDA = 0, 1, 2, 3
 PKV_F16, PKV_F32, PKV_F64, PKV_BF16 = 1, 2, 3, 4
@@ -64,7 +60,7 @@ PROTOTYPES = {
     "pkv_cache_reserve": (C.c_int, [_vp, _i64, _i32, _vp]),
     "pkv_cache_reset": (C.c_int, [_vp, _i32, _vp]),
     "pkv_check_finite": (C.c_int, [_vp, _i32, _i64, _P(_i64), _vp]),
-    "pkv_mine": (C.c_int, [_vp, _i32, _vp, _i64, _P(_i64), _P(_f64), _P(_i32), _vp]),
+    "pkv_mine": (C.c_int, [_vp, _i32, _vp, _i64, _P(_i64), _P(_f64), _P(_i32), _vp, _vp]),
     "pkv_set_patterns": (C.c_int, [_vp, _i32, _vp, _i32, _vp]),
     "pkv_prefill": (C.c_int, [_vp, _vp, _vp, _i64, _P(_i64), _P(_i64), _vp]),
     "pkv_append": (C.c_int, [_vp, _vp, _vp, _vp]),
@@ -83,15 +79,29 @@ PROTOTYPES = {
     "pkv_kmeans": (C.c_int, [_vp, _i64, _i32, _i32, _i64, _vp, _vp, _P(_f64), _P(_i32), _P(_i32), _vp]),
 }
 
-for _name, (_res, _args) in PROTOTYPES.items():
-    _fn = getattr(lib, _name)  # AttributeError here = the .so does not export a declared symbol
-    _fn.restype = _res
-    _fn.argtypes = _args
+
+def load():
+    """Load libpkv_b200.so and bind every prototype; ImportError when it is missing."""
+    global lib
+    if lib is not None:
+        return lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2510_05176_b200.build` "
+            "(the B200 codec has no CPU fallback)"
+        )
+    handle = C.CDLL(LIB_PATH)
+    for name, (res, args) in PROTOTYPES.items():
+        fn = getattr(handle, name)  # AttributeError here = the .so does not export a declared symbol
+        fn.restype = res
+        fn.argtypes = args
+    lib = handle
+    return lib
 
 
 def last_error() -> tuple[str, int]:
     idx = C.c_int64(-1)
-    msg = lib.pkv_last_error(C.byref(idx))
+    msg = load().pkv_last_error(C.byref(idx))
     return (msg.decode() if msg else ""), idx.value
 
 
@@ -108,4 +118,4 @@ def check(rc: int) -> None:
 
 
 def call(name: str, *args) -> None:
-    check(getattr(lib, name)(*args))
+    check(getattr(load(), name)(*args))

@@ -103,14 +103,18 @@ class PatternKVCache:
                   C.byref(h))
         self._h = h
         self.record_decisions = record_decisions
-        self.n_prefill_patterns = (0, 0)
-        self.first_decision_token = 0  # committed tokens before this have no gate record
+        # per-unit pattern counts right after the last prefill (device snapshot, read lazily so
+        # prefill never blocks the host) and the committed count at that point
+        self._npre_dev = None
+        self._npre = (np.zeros(n_units, np.int64), np.zeros(n_units, np.int64))
+        self._prefill_committed = 0
+        self._first_decision = None
         self._part = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _lib.lib.pkv_cache_destroy(h)
+            _lib.load().pkv_cache_destroy(h)
             self._h = None
 
     # ---- introspection --------------------------------------------------------
@@ -172,9 +176,44 @@ class PatternKVCache:
         if mine and cfg.use_v_patterns:
             fv = (C.c_int64 * self.n_units)(*([first_seed_index(T, cfg.seed + 1)] * self.n_units))
         _lib.call("pkv_prefill", self._h, _ptr(k), _ptr(v), T, fk, fv, _stream())
-        self.n_prefill_patterns = self.pattern_counts_max()
-        if (cfg.use_v_patterns and self.n_prefill_patterns[1] == 0):
-            self.first_decision_token = self.info().committed_count
+        # stream-ordered device copies of the per-unit counts: no host synchronisation here
+        self._npre_dev = (self.read("nk", torch.int32, (self.n_units,)), self.read("nv", torch.int32, (self.n_units,)))
+        self._prefill_committed = T - min(T, cfg.residual_window)
+        self._first_decision = None
+
+    # ---- prefill bookkeeping (read lazily) ------------------------------------------------
+    @property
+    def prefill_pattern_counts(self):
+        """Per-unit (K, V) pattern counts as of the last prefill / restore: patterns below these
+        indices have origin "prefill", the rest "decode" (patterns.py:25-60 origins)."""
+        if self._npre_dev is not None:
+            self._npre = tuple(t.cpu().numpy().astype(np.int64) for t in self._npre_dev)
+            self._npre_dev = None
+        return self._npre
+
+    @prefill_pattern_counts.setter
+    def prefill_pattern_counts(self, counts):
+        self._npre_dev = None
+        self._npre = tuple(np.asarray(c, np.int64).reshape(self.n_units) for c in counts)
+
+    @property
+    def n_prefill_patterns(self):
+        """Largest per-unit prefill pattern count per side."""
+        nk, nv = self.prefill_pattern_counts
+        return int(nk.max(initial=0)), int(nv.max(initial=0))
+
+    @property
+    def first_decision_token(self) -> int:
+        """Committed tokens before this index carry no gate record (V had no patterns yet)."""
+        if self._first_decision is not None:
+            return self._first_decision
+        if self.config.use_v_patterns and self.n_prefill_patterns[1] == 0:
+            return self._prefill_committed
+        return 0
+
+    @first_decision_token.setter
+    def first_decision_token(self, t: int):
+        self._first_decision = int(t)
 
     def reset(self, keep_patterns: bool = True) -> None:
         """Empty the cache (token_count = 0); keep the pattern tables for a re-prefill."""
@@ -199,16 +238,19 @@ class PatternKVCache:
             raise DataError(f"non-finite decode vector at token {self.info().token_count}")
         _lib.call("pkv_append", self._h, _ptr(k), _ptr(v), _stream())
 
-    def mine(self, side: int, x: torch.Tensor, seed: int):
-        """mine_patterns for every unit (patterns.py:145-158); returns (history [U, 25], niter [U])."""
+    def mine(self, side: int, x: torch.Tensor, seed: int, labels: bool = False):
+        """mine_patterns for every unit (patterns.py:145-158); returns (history [U, 25], niter [U])
+        and, with labels=True, the final assignment [U, T] int32 on the device (patterns.py:84-85)."""
         x = self._as_input(x, 3, "mining input")
         T = x.shape[1]
         first = (C.c_int64 * self.n_units)(*([first_seed_index(T, seed)] * self.n_units))
         hist = np.zeros((self.n_units, 25))
         nit = np.zeros(self.n_units, np.int32)
+        lab = torch.empty((self.n_units, T), dtype=torch.int32, device="cuda") if labels else None
         _lib.call("pkv_mine", self._h, side, _ptr(x), T, first,
-                  hist.ctypes.data_as(C.POINTER(C.c_double)), nit.ctypes.data_as(C.POINTER(C.c_int32)), _stream())
-        return hist, nit
+                  hist.ctypes.data_as(C.POINTER(C.c_double)), nit.ctypes.data_as(C.POINTER(C.c_int32)), _ptr(lab),
+                  _stream())
+        return (hist, nit, lab) if labels else (hist, nit)
 
     # ---- reads --------------------------------------------------------------------------
     def decode_attention(self, q: torch.Tensor, sm_scale: float | None = None, out: torch.Tensor | None = None):

@@ -36,7 +36,7 @@ class EngineConfig:
         from .cache import make_config_struct
 
         s = make_config_struct(self)
-        _lib.check(_lib.lib.pkv_config_validate(C.byref(s)))
+        _lib.check(_lib.load().pkv_config_validate(C.byref(s)))
 
     def raw_variant(self) -> "EngineConfig":
         """Same geometry with every pattern mechanism disabled (engine.py:77-79)."""

@@ -138,6 +138,7 @@ struct pkv_cache {
   unsigned long long* scratch_flag = nullptr;
   int64_t uploaded_nbcap = -1, uploaded_base = -1;   // last block table sent to the device
   std::vector<int64_t> uploaded_start;
+  bool blocks_stale = false;   // reset dropped the prefill geometry; re-upload before the next flush
 };
 
 static int esize_of(int dtype) {
@@ -333,6 +334,12 @@ extern "C" int pkv_cache_reset(pkv_cache* c, int32_t keep_patterns, void* stream
   c->win_len = 0;
   c->win_slot0 = 0;
   c->nb = 0;
+  // the next flush (without a prefill) starts a fresh block table at token 0
+  c->blk_start.clear();
+  c->blk_len.clear();
+  c->nb_prefill = 0;
+  c->decode_base = 0;
+  c->blocks_stale = true;
   if (!keep_patterns) {
     CU(cudaMemsetAsync(c->dev.nk, 0, (size_t)c->U * 4, st));
     CU(cudaMemsetAsync(c->dev.nv, 0, (size_t)c->U * 4, st));
@@ -424,7 +431,7 @@ static cudaError_t dispatch(int dtype, F&& f) {
 // mining (patterns.py:145-158 per unit)
 // ---------------------------------------------------------------------------------
 static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv, int64_t T, const int64_t* fk,
-                     const int64_t* fv, double* hist_host, int32_t* niter_host, cudaStream_t st) {
+                     const int64_t* fv, double* hist_host, int32_t* niter_host, int32_t* labels_dev, cudaStream_t st) {
   const int U = c->U, k = c->cfg.pattern_count;
   if (T < 1) return fail(PKV_USAGE, -1, "pattern mining expects a non-empty 2-D array of row vectors");
   for (int s = 0; s < 2; ++s) {
@@ -439,6 +446,8 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
   double *near_ = nullptr, *own = nullptr, *hist = nullptr;
   int *lab = nullptr, *lab2 = nullptr, *list = nullptr, *niter = nullptr;
   int64_t* first = nullptr;
+  int* lab_out = nullptr;
+  if (labels_dev) CU(cudaMallocAsync((void**)&lab_out, n2 * 4, st));
   CU(cudaMallocAsync((void**)&near_, n2 * 8, st));
   CU(cudaMallocAsync((void**)&own, n2 * 8, st));
   CU(cudaMallocAsync((void**)&lab, n2 * 4, st));
@@ -461,10 +470,16 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
     a.first[0] = first; a.first[1] = first + U;
     a.k = k; a.side_mask = side_mask;
     a.near_ = near_; a.own = own; a.lab = lab; a.lab2 = lab2; a.list = list;
-    a.hist = hist; a.niter = niter; a.labels_out = nullptr;
+    a.hist = hist; a.niter = niter; a.labels_out = lab_out;
     return launch_mine<T_>(c->dev, a, st);
   });
   CU(e);
+  if (labels_dev) {  // [U][2][T] -> the mined side's [U][T]
+    const int s = (side_mask & 1) ? 0 : 1;
+    CU(cudaMemcpy2DAsync(labels_dev, (size_t)T * 4, lab_out + (size_t)s * T, (size_t)2 * T * 4, (size_t)T * 4, U,
+                         cudaMemcpyDeviceToDevice, st));
+    CU(cudaFreeAsync(lab_out, st));
+  }
   if (hist_host || niter_host) {
     std::vector<double> hh((size_t)U * 2 * 25);
     std::vector<int> nh((size_t)U * 2);
@@ -486,10 +501,10 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
 }
 
 extern "C" int pkv_mine(pkv_cache* c, int32_t side, const void* x, int64_t T, const int64_t* first_idx, double* history,
-                        int32_t* niter, void* stream) {
+                        int32_t* niter, int32_t* labels, void* stream) {
   if (!c || !x || !first_idx) return fail(PKV_USAGE, -1, "null argument");
   if (side != 0 && side != 1) return fail(PKV_USAGE, -1, "side must be 0 (K) or 1 (V)");
-  return mine_impl(c, 1 << side, x, x, T, first_idx, first_idx, history, niter, (cudaStream_t)stream);
+  return mine_impl(c, 1 << side, x, x, T, first_idx, first_idx, history, niter, labels, (cudaStream_t)stream);
 }
 
 // pattern tables with per-unit counts (device [U][P][D] fp64, host counts [U] <= P)
@@ -570,6 +585,7 @@ extern "C" int pkv_cache_import(pkv_cache* c, int64_t token_count, int32_t nb, c
   c->decode_base = nb_prefill > 0 ? blk_start[nb_prefill - 1] + blk_len[nb_prefill - 1] : 0;
   rc = upload_blocks(c, st);
   if (rc) return rc;
+  c->blocks_stale = false;
   CU(launch_import(d, nb, C, kparam, kidx, vidx, vparam, kcodes, vcodes, kdiag, vdiag, st));
   if (win_len > 0) {
     const size_t row = (size_t)c->D * c->esize;
@@ -639,7 +655,7 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
   if (cfg.use_k_patterns && first_k) mask |= 1;
   if (cfg.use_v_patterns && first_v) mask |= 2;
   if (mask) {
-    rc = mine_impl(c, mask, k, v, T, first_k, first_v, nullptr, nullptr, st);
+    rc = mine_impl(c, mask, k, v, T, first_k, first_v, nullptr, nullptr, nullptr, st);
     if (rc) return rc;
   }
   // block geometry (engine.py:161-165): spans of G from 0, short tail allowed
@@ -653,6 +669,7 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
   c->decode_base = commit_n;
   rc = upload_blocks(c, st);
   if (rc) return rc;
+  c->blocks_stale = false;
   cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
     using T_ = std::remove_pointer_t<decltype(tp)>;
     SpanSrc<T_> sk{(const T_*)k, T * c->D, 0, INT64_MAX / 4};
@@ -687,6 +704,11 @@ extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stre
   const pkv_config& cfg = c->cfg;
   const int W = cfg.residual_window, G = cfg.group_size;
   DevCache& d = c->dev;
+  if (c->blocks_stale) {
+    int rc = upload_blocks(c, st);
+    if (rc) return rc;
+    c->blocks_stale = false;
+  }
   const int slot = (c->win_slot0 + c->win_len) % d.Wcap;
   cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
     using T_ = std::remove_pointer_t<decltype(tp)>;

@@ -76,6 +76,7 @@ def export_unit(cache: PatternKVCache, u: int, with_bytes: bool = True) -> UnitS
     D = cache.head_dim
     Cn = inf.committed_count
     nk, nv = cache.pattern_counts()
+    npre_k, npre_v = cache.prefill_pattern_counts
     kpat = cache.patterns(0)[u, : nk[u]].cpu().numpy() if cfg.use_k_patterns else np.zeros((0, D))
     vpat = cache.patterns(1)[u, : nv[u]].cpu().numpy() if cfg.use_v_patterns else np.zeros((0, D))
     kb_start, kb_len = cache.block_table()
@@ -110,7 +111,7 @@ def export_unit(cache: PatternKVCache, u: int, with_bytes: bool = True) -> UnitS
         vrows = pack_rows(vc_u, cfg.bits).cpu().numpy()
         v_bytes = [vrows[t].tobytes() for t in range(Cn)]
     return UnitState(
-        kpat=kpat, vpat=vpat, n_prefill_k=cache.n_prefill_patterns[0], n_prefill_v=cache.n_prefill_patterns[1],
+        kpat=kpat, vpat=vpat, n_prefill_k=int(npre_k[u]), n_prefill_v=int(npre_v[u]),
         kb_start=np.asarray(kb_start, np.int64), kb_len=np.asarray(kb_len, np.int64),
         k_scale=kp[:, 0, :], k_zero=kp[:, 1, :], k_codes=kc_u.cpu().numpy(), k_idx=kidx,
         v_scale=vp[:, 0], v_zero=vp[:, 1], v_codes=vc_u.cpu().numpy(), v_idx=vidx,

@@ -443,9 +443,7 @@ def restore_cache(states: dict, dtype=None, max_tokens: int | None = None, recor
               _ptr(t_kd), _ptr(t_vd), _stream())
     npk = [sum(st.k_patterns.origin(i) == ORIGIN_PREFILL for i in range(len(st.k_patterns))) for st in sts]
     npv = [sum(st.v_patterns.origin(i) == ORIGIN_PREFILL for i in range(len(st.v_patterns))) for st in sts]
-    if len(set(npk)) > 1 or len(set(npv)) > 1:
-        raise UsageError("restored heads must share their prefill pattern counts")
-    cache.n_prefill_patterns = (npk[0], npv[0])
+    cache.prefill_pattern_counts = (npk, npv)
     torch.cuda.synchronize()
     return cache, keys
 

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     syms = declared_symbols()
     assert len(syms) >= 20
     for s in syms:
-        assert hasattr(_lib.lib, s), s
+        assert hasattr(_lib.load(), s), s
         assert s in _lib.PROTOTYPES, f"{s} has no ctypes prototype"
 
 
@@ -99,6 +99,23 @@ def test_no_device_fails_loudly():
 
     h = C.c_void_p()
     s = make_config_struct(P.EngineConfig())
-    rc = _lib.lib.pkv_cache_create(C.byref(s), 1, 128, _lib.PKV_F16, 1024, 64, 0, C.byref(h))
+    rc = _lib.load().pkv_cache_create(C.byref(s), 1, 128, _lib.PKV_F16, 1024, 64, 0, C.byref(h))
     assert rc == _lib.PKV_USAGE
     assert "no CUDA device" in _lib.last_error()[0]
+
+
+def test_import_fails_loudly_without_library_and_build_module_runs_from_clean_tree():
+    """No CPU fallback: importing the package without libpkv_b200.so raises ImportError;
+    `python -m paper_2510_05176_b200.build` does not need the library to exist."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, PKV_LIB="/nonexistent/libpkv_b200.so")
+    r = subprocess.run([sys.executable, "-c", "import paper_2510_05176_b200"], cwd=ROOT, env=env,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr
+    # the package __init__ skips the eager load only for the build module run as __main__
+    r = subprocess.run([sys.executable, "-c", "import sys; sys.orig_argv = ['python', '-m', "
+                        "'paper_2510_05176_b200.build']; import paper_2510_05176_b200; print('ok')"],
+                       cwd=ROOT, env=env, capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr

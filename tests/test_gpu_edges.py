@@ -221,3 +221,31 @@ def test_long_context_cfg3_length(pkv, monkeypatch):
         del cache
     for a, b in zip(res[0], res[1]):
         assert torch.equal(a, b)
+
+
+def test_reset_then_decode_only(pkv):
+    """pkv_cache_reset after a prefill with a short tail block, then decode appends with no new
+    prefill: the first flush starts a fresh block table at token 0 (no stale prefill geometry)
+    and equals an oracle head that holds the same pattern tables and only appends."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    d, tp, steps = 128, 700, 300  # 572 committed = 4 full blocks + a 60-token tail
+    k, v = _units(2, tp + steps, d, seed=21)
+    cfg = dict(bits=2, pattern_count=16)
+    cache = pkv.PatternKVCache(EngineConfig(**cfg), 2, d, dtype=torch.float16, max_tokens=1024)
+    kt = torch.from_numpy(k).half().cuda()
+    vt = torch.from_numpy(v).half().cuda()
+    cache.prefill(kt[:, :tp], vt[:, :tp])
+    pats = [cache.patterns(s)[:, :16].cpu().numpy() for s in (0, 1)]
+    cache.reset(keep_patterns=True)
+    for t in range(tp, tp + steps):
+        cache.append(kt[:, t], vt[:, t])
+    heads = []
+    for u in range(2):
+        h = O.OracleHead(O.Knobs(**cfg), d)
+        h.kpat, h.vpat = pats[0][u].copy(), pats[1][u].copy()
+        for t in range(tp, tp + steps):
+            h.append(k[u, t], v[u, t])
+        heads.append(h)
+    assert cache.info().n_blocks == 1 and cache.block_table()[0].tolist() == [0]
+    _assert_matches_oracle(cache, heads)

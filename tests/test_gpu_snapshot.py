@@ -106,3 +106,42 @@ def test_resume_decoding_matches_oracle(gold, name):
         h = O.replay(k[i, :tp], v[i, :tp], np.concatenate([k[i, tp:], ke[i]]), np.concatenate([v[i, tp:], ve[i]]), knobs)
         parts.append(snapshot._unit_bytes(heads[i][0], heads[i][1], _OracleUnit(h, cfg.bits), cfg.bits, d))
     assert got == b"".join(parts)
+
+
+def test_mixed_prefill_pattern_counts():
+    """Units that mine different numbers of patterns (one has only 5 distinct rows, so
+    patterns.py:95-101 returns 5 centroids) keep per-unit origin tags: the decode-appended
+    patterns of the short unit are tagged "decode" from index 5 on, the image equals the
+    oracle-built one, and it restores and round-trips."""
+    import paper_2510_05176_b200 as P
+    from paper_2510_05176_b200 import snapshot
+    from test_snapshot import _OracleUnit
+
+    d, tp, td = 64, 512, 300
+    kw = dict(bits=2, pattern_count=16, group_size=128, residual_window=128)
+    k0, v0 = O.synth_unit(O.unit_seed(1, 2, 3), tp + td, d)
+    k1, v1 = O.synth_unit(O.unit_seed(4, 5, 6), tp + td, d)
+    rows = np.random.default_rng(3).integers(0, 5, size=tp)
+    k1[:tp] = k1[rows]
+    v1[:tp] = v1[rows]
+    k = np.stack([k0, k1]).astype(np.float16).astype(np.float64)
+    v = np.stack([v0, v1]).astype(np.float16).astype(np.float64)
+    cfg = P.EngineConfig(**kw)
+    cache = P.PatternKVCache(cfg, 2, d, dtype=torch.float64, max_tokens=tp + td + 256, record_decisions=True)
+    kt, vt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    cache.prefill(kt[:, :tp], vt[:, :tp])
+    for t in range(tp, tp + td):
+        cache.append(kt[:, t], vt[:, t])
+    npk, npv = cache.prefill_pattern_counts
+    assert list(npk) == [16, 5] and list(npv) == [16, 5]
+    keys = [(0, 0), (0, 1)]
+    got = snapshot.cache_snapshot_bytes(cache, keys)
+    knobs = O.Knobs(**kw)
+    parts = [snapshot._header(cfg, d, 2)]
+    for i in range(2):
+        h = O.replay(k[i, :tp], v[i, :tp], k[i, tp:], v[i, tp:], knobs)
+        parts.append(snapshot._unit_bytes(0, i, _OracleUnit(h, cfg.bits), cfg.bits, d))
+    assert got == b"".join(parts)
+    _, states = snapshot.parse_snapshot(got)
+    cache2, keys2 = snapshot.restore_cache(states, dtype=torch.float64)
+    assert snapshot.cache_snapshot_bytes(cache2, keys2) == got
