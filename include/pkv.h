@@ -126,6 +126,22 @@ int pkv_append(pkv_cache* c, const void* k, const void* v, void* stream);
  * [U][gqa][D]. */
 int pkv_decode_attn(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, float* out, void* stream);
 
+/* Partial decode attention for a sequence split across ranks (new; SURVEY 8e,
+ * cfg3 at 8 GPUs): attention over committed blocks [blk0, blk1) plus the exact
+ * window when with_window != 0, returned unnormalised: o device fp32 [U][gqa][D]
+ * = sum_t e^(s_t - m) v_t, ml device fp32 [U][gqa][2] = (m, l = sum_t e^(s_t - m)),
+ * s_t = sm_scale q.k_t (natural-log units; m = -inf, l = 0 for an empty range).
+ * Ranks exchange (o, m, l) once and LSE-merge (dist.gather_and_merge_partials). */
+int pkv_decode_attn_partial(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, int32_t blk0, int32_t blk1,
+                            int32_t with_window, float* o, float* ml, void* stream);
+
+/* Fork units (new; parallel sampling from one prompt, BASELINE configs[3]): unit
+ * dst_units[i] becomes a copy of unit src_units[i] -- pattern tables, committed
+ * codes/params/indices, gate records and window (all units share the token count
+ * and block geometry, so a copy is a whole state).  The reference equivalent is
+ * copy.deepcopy of a HeadCacheState (engine.py:104-129).  Host arrays [n]. */
+int pkv_cache_fork(pkv_cache* c, const int32_t* src_units, const int32_t* dst_units, int32_t n, void* stream);
+
 /* committed_matrices / reconstruct_token (engine.py:271-303), exact fp64:
  * committed tokens [t0, t1) -> device [U][t1-t0][D] each. */
 int pkv_dequant(pkv_cache* c, int64_t t0, int64_t t1, double* k_out, double* v_out, void* stream);

@@ -65,6 +65,8 @@ PROTOTYPES = {
     "pkv_prefill": (C.c_int, [_vp, _vp, _vp, _i64, _P(_i64), _P(_i64), _vp]),
     "pkv_append": (C.c_int, [_vp, _vp, _vp, _vp]),
     "pkv_decode_attn": (C.c_int, [_vp, _vp, _i32, _f32, _vp, _vp]),
+    "pkv_decode_attn_partial": (C.c_int, [_vp, _vp, _i32, _f32, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "pkv_cache_fork": (C.c_int, [_vp, _P(_i32), _P(_i32), _i32, _vp]),
     "pkv_dequant": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "pkv_export_codes": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "pkv_cache_import": (C.c_int, [_vp, _i64, _i32, _P(_i64), _P(_i32), _i32, _i32, _i32, _i32, _P(_i32), _P(_i32),

@@ -266,6 +266,40 @@ class PatternKVCache:
         _lib.call("pkv_decode_attn", self._h, _ptr(q), q.shape[1], C.c_float(sm_scale), _ptr(out), _stream())
         return out
 
+    def decode_attention_partial(self, q: torch.Tensor, blk0: int = 0, blk1: int | None = None,
+                                 with_window: bool = True, sm_scale: float | None = None):
+        """Unnormalised attention over committed blocks [blk0, blk1) (+ the exact window) for a
+        sequence split across ranks: returns (o [U, G, D], m [U, G], l [U, G]) fp32 with
+        o = sum_t e^(s_t - m) v_t and l = sum_t e^(s_t - m) (natural-log units); merge the
+        ranks' partials with dist.gather_and_merge_partials."""
+        if q.dim() != 3 or q.shape[0] != self.n_units or q.shape[2] != self.head_dim:
+            raise UsageError("q must have shape [n_units, G, head_dim]")
+        q = q.to(device="cuda", dtype=torch.float32).contiguous()
+        if sm_scale is None:
+            sm_scale = 1.0 / float(np.sqrt(self.head_dim))
+        if blk1 is None:
+            blk1 = self.info().n_blocks
+        o = torch.empty_like(q)
+        ml = torch.empty((self.n_units, q.shape[1], 2), dtype=torch.float32, device="cuda")
+        _lib.call("pkv_decode_attn_partial", self._h, _ptr(q), q.shape[1], C.c_float(sm_scale), int(blk0), int(blk1),
+                  int(bool(with_window)), _ptr(o), _ptr(ml), _stream())
+        return o, ml[..., 0], ml[..., 1]
+
+    def fork(self, src_units, dst_units) -> None:
+        """Unit dst_units[i] becomes a copy of unit src_units[i] (parallel samples of one prompt)."""
+        src = [int(x) for x in src_units]
+        dst = [int(x) for x in dst_units]
+        if len(src) != len(dst):
+            raise UsageError("fork needs as many source as destination units")
+        n = len(src)
+        _lib.call("pkv_cache_fork", self._h, (C.c_int32 * max(n, 1))(*src), (C.c_int32 * max(n, 1))(*dst), n,
+                  _stream())
+        if self._npre_dev is not None:
+            self.prefill_pattern_counts  # materialise before remapping  # noqa: B018
+        nk, nv = (c.copy() for c in self._npre)
+        nk[dst], nv[dst] = nk[src], nv[src]
+        self._npre = (nk, nv)
+
     def dequant(self, t0: int = 0, t1: int | None = None):
         """Exact fp64 reconstruction of committed tokens [t0, t1): ([U,n,D], [U,n,D])."""
         if t1 is None:

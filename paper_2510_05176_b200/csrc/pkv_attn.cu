@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
                 : sW + ((size_t)warp * max(Pv, 1) + p) * MAXG + 4 * nt + qd;
   };
 
-  const int b0 = chunk * a.bpc;
-  const int b1 = min(a.nb, b0 + a.bpc);
+  const int b0 = a.blk0 + chunk * a.bpc;
+  const int b1 = min(a.blk0 + a.nb, b0 + a.bpc);
   // ---- register-prefetched tile stream: the lane's 16*BITS/8 code words per side come
   // straight from HBM (fragment order makes them one contiguous vector per lane) while the
   // previous tile computes; metadata: kidx / vidx / vparam of tokens g, g+8
@@ -538,8 +538,17 @@ __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_s
     for (int j = 0; j < 4; ++j) o[j] = o[j] * al + (lane + 32 * j < Dp ? pp[lane + 32 * j] * be : 0.f);
     m = mn;
   }
-  const float inv = 1.f / l;
   float* dst = out + ((int64_t)u * a.G + h) * D;
+  if (a.ml) {  // partial (o, m, l) for a cross-rank LSE merge: m in natural-log units
+#pragma unroll
+    for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) dst[lane + 32 * j] = o[j];
+    if (lane == 0) {
+      a.ml[((int64_t)u * a.G + h) * 2] = m * 0.6931471805599453f;
+      a.ml[((int64_t)u * a.G + h) * 2 + 1] = l;
+    }
+    return;
+  }
+  const float inv = 1.f / l;
 #pragma unroll
   for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) dst[lane + 32 * j] = o[j] * inv;
 }
@@ -553,7 +562,9 @@ size_t attn_smem_bytes(int Dp, int Pk, int Pv, int bits, int NT) {
 
 template <int BITS, int NT, int KT>
 static cudaError_t launch_chunks_kt(const DevCache& c, const AttnArgs& a, size_t smem, cudaStream_t st) {
-  cudaFuncSetAttribute(attn_chunk_kernel<BITS, NT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<BITS, NT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+  if (e != cudaSuccess) return e;
   attn_chunk_kernel<BITS, NT, KT><<<dim3(a.nchunk, c.U), ATT_THREADS, smem, st>>>(c, a);
   return cudaGetLastError();
 }
@@ -572,6 +583,7 @@ cudaError_t launch_attn(const DevCache& c, const AttnArgs& a, int Pk_max, int Pv
   if (a.nb > 0) {
     const int nt = a.G <= 4 ? 1 : 2;
     size_t smem = attn_smem_bytes(c.Dp, Pk_max, Pv_max, c.bits, nt);
+    if (smem > 227 * 1024) return cudaErrorNotSupported;  // pkv_decode_attn reports the pattern-count limit
     if (c.bits == 2) e = nt == 1 ? launch_chunks<2, 1>(c, a, smem, st) : launch_chunks<2, 2>(c, a, smem, st);
     else if (c.bits == 4) e = nt == 1 ? launch_chunks<4, 1>(c, a, smem, st) : launch_chunks<4, 2>(c, a, smem, st);
     else e = nt == 1 ? launch_chunks<8, 1>(c, a, smem, st) : launch_chunks<8, 2>(c, a, smem, st);

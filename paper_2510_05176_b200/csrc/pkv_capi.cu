@@ -290,6 +290,15 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
   }
   rc = reserve(c, std::max<int64_t>(max_tokens, 1), std::max(max_patterns, cfg->pattern_count + 8), st);
   if (rc) return bail(rc);
+  {  // decode-attention chunk partials, sized once for the largest chunking attn_impl picks
+    // (U * nchunk <= 16 * SMs + U) and 8 query heads, so decode steps never allocate
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    c->part_bytes = (size_t)(16 * std::max(nsm, 1) + n_units) * 8 * (c->Dp + 2) * 4;
+    if (cudaMalloc((void**)&c->part, c->part_bytes) != cudaSuccess)
+      return bail(fail(PKV_CUDA, -1, "cudaMalloc of %zu attention partial bytes failed", c->part_bytes));
+  }
   *out = c;
   return PKV_OK;
 }
@@ -760,11 +769,13 @@ extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stre
 // ---------------------------------------------------------------------------------
 // decode attention
 // ---------------------------------------------------------------------------------
-extern "C" int pkv_decode_attn(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, float* out, void* stream) {
+static int attn_impl(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, int32_t blk0, int32_t blk1,
+                     int32_t with_window, float* out, float* ml, cudaStream_t st) {
   if (!c || !q || !out) return fail(PKV_USAGE, -1, "null argument");
   if (gqa < 1 || gqa > 8) return fail(PKV_USAGE, -1, "query heads per KV head must lie in [1, 8], got %d", gqa);
   if (c->token_count == 0) return fail(PKV_USAGE, -1, "attention over an empty cache");
-  cudaStream_t st = (cudaStream_t)stream;
+  if (blk0 < 0 || blk1 > c->nb || blk0 > blk1)
+    return fail(PKV_USAGE, blk0, "block range [%d, %d) outside the %d committed blocks", blk0, blk1, c->nb);
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -773,25 +784,85 @@ extern "C" int pkv_decode_attn(pkv_cache* c, const float* q, int32_t gqa, float 
     if (num_sms <= 0) num_sms = 148;
   }
   AttnArgs a;
-  a.q = q; a.G = gqa; a.scale_log2 = sm_scale * 1.4426950408889634f; a.nb = c->nb;
+  a.q = q; a.G = gqa; a.scale_log2 = sm_scale * 1.4426950408889634f;
+  a.blk0 = blk0; a.nb = blk1 - blk0; a.ml = ml;
   // enough CTAs for ~4 waves at 4 CTAs/SM, >= 4 blocks per chunk (one per warp)
   const int target = 16 * num_sms;
-  int nchunk = std::max(1, std::min((target + c->U - 1) / c->U, (c->nb + 3) / 4));
-  a.bpc = std::max(1, (c->nb + nchunk - 1) / nchunk);
-  a.nchunk = std::max(1, (c->nb + a.bpc - 1) / a.bpc);
+  int nchunk = std::max(1, std::min((target + c->U - 1) / c->U, (a.nb + 3) / 4));
+  a.bpc = std::max(1, (a.nb + nchunk - 1) / nchunk);
+  a.nchunk = std::max(1, (a.nb + a.bpc - 1) / a.bpc);
   const size_t need = (size_t)c->U * a.nchunk * gqa * (c->Dp + 2) * 4;
   if (need > c->part_bytes) {
-    if (c->part) cudaFree(c->part);
+    if (c->part) { CU(cudaStreamSynchronize(st)); cudaFree(c->part); c->part = nullptr; c->part_bytes = 0; }
     CU(cudaMalloc((void**)&c->part, need));
     c->part_bytes = need;
   }
   a.part = c->part;
   const int pk = c->cfg.use_k_patterns ? c->pk_bound : 0, pv = c->cfg.use_v_patterns ? c->pv_bound : 0;
+  const int wl = with_window ? c->win_len : 0;
   cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
     using T_ = std::remove_pointer_t<decltype(tp)>;
-    return launch_attn<T_>(c->dev, a, pk, pv, c->win_len, c->win_slot0, out, st);
+    return launch_attn<T_>(c->dev, a, pk, pv, wl, c->win_slot0, out, st);
   });
+  if (e == cudaErrorNotSupported)
+    return fail(PKV_USAGE, -1, "decode attention holds the q.M table and pattern weights in shared memory: %d K / %d V "
+                "patterns exceed its 227 KB (about 1100 patterns per side)", pk, pv);
   CU(e);
+  return PKV_OK;
+}
+
+extern "C" int pkv_decode_attn(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, float* out, void* stream) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  return attn_impl(c, q, gqa, sm_scale, 0, c->nb, 1, out, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int pkv_decode_attn_partial(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, int32_t blk0,
+                                       int32_t blk1, int32_t with_window, float* o, float* ml, void* stream) {
+  if (!c || !ml) return fail(PKV_USAGE, -1, "null argument");
+  return attn_impl(c, q, gqa, sm_scale, blk0, blk1, with_window, o, ml, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------------
+// unit fork (parallel sampling from one prompt: a unit's whole state copied)
+// ---------------------------------------------------------------------------------
+extern "C" int pkv_cache_fork(pkv_cache* c, const int32_t* src_units, const int32_t* dst_units, int32_t n,
+                              void* stream) {
+  if (!c || (n > 0 && (!src_units || !dst_units))) return fail(PKV_USAGE, -1, "null argument");
+  if (n < 0) return fail(PKV_USAGE, -1, "negative unit count");
+  std::vector<int> hs(n), hd(n), seen(c->U, 0);
+  for (int i = 0; i < n; ++i) {
+    if (src_units[i] < 0 || src_units[i] >= c->U || dst_units[i] < 0 || dst_units[i] >= c->U)
+      return fail(PKV_USAGE, i, "fork pair %d (%d -> %d) outside the %d units", i, src_units[i], dst_units[i], c->U);
+    if (seen[dst_units[i]]++) return fail(PKV_USAGE, i, "unit %d is a fork destination twice", dst_units[i]);
+    hs[i] = src_units[i];
+    hd[i] = dst_units[i];
+  }
+  for (int i = 0; i < n; ++i)
+    if (seen[hs[i]] && hs[i] != hd[i])
+      return fail(PKV_USAGE, i, "unit %d is both a fork source and a destination", hs[i]);
+  if (n == 0) return PKV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const DevCache& d = c->dev;
+  const int64_t P = d.Pcap, NB = d.NBcap, T = d.Tcap, D = c->D, Dp = c->Dp;
+  ForkArenas fa;
+  std::memset(&fa, 0, sizeof fa);
+  auto add = [&](void* p, int64_t bytes) { fa.a[fa.n].base = (unsigned char*)p; fa.a[fa.n].unit_bytes = p ? bytes : 0; ++fa.n; };
+  add(d.kpat64, P * D * 8); add(d.vpat64, P * D * 8); add(d.kpat32, P * Dp * 4); add(d.vpat32, P * Dp * 4);
+  add(d.kpmax, 4); add(d.vpmax, 4); add(d.nk, 4); add(d.nv, 4); add(d.probe, 2 * 16 * 4);
+  add(d.kcodes, NB * d.blk_bytes); add(d.vcodes, NB * d.blk_bytes);
+  add(d.kparam32, NB * 2 * Dp * 4); add(d.kparam64, NB * 2 * D * 8);
+  add(d.kidx, NB * d.GP * 2); add(d.vidx, NB * d.GP * 2); add(d.vparam32, NB * d.GP * 8);
+  add(d.vparam64, T * 16);
+  if (d.keep_diag) { add(d.kdiag, T * 16); add(d.vdiag, T * 16); }
+  add(d.wk, (int64_t)d.Wcap * D * c->esize); add(d.wv, (int64_t)d.Wcap * D * c->esize);
+  int* dev_pairs = nullptr;
+  CU(cudaMallocAsync((void**)&dev_pairs, (size_t)2 * n * 4, st));
+  std::vector<int> pairs(hs);
+  pairs.insert(pairs.end(), hd.begin(), hd.end());
+  CU(cudaMemcpyAsync(dev_pairs, pairs.data(), (size_t)2 * n * 4, cudaMemcpyHostToDevice, st));
+  CU(launch_fork(fa, n, dev_pairs, dev_pairs + n, st));
+  CU(cudaFreeAsync(dev_pairs, st));
+  CU(cudaStreamSynchronize(st));  // the host pair list must outlive the async copy
   return PKV_OK;
 }
 

@@ -228,9 +228,18 @@ struct AttnArgs {
   const float* q;      // [U][G][D] fp32
   int G;               // query heads per unit
   float scale_log2;    // sm_scale * log2(e)
-  int nb;              // committed blocks
+  int blk0;            // first committed block attended (sequence split: a rank's block range)
+  int nb;              // committed blocks attended, [blk0, blk0 + nb)
   int nchunk, bpc;     // chunks per unit, blocks per chunk
   float* part;         // [U][nchunk][G][Dp + 2]  (o[Dp], m, l)
+  float* ml;           // partial mode: [U][G][2] (m in natural-log units, l); out = unnormalised o
+};
+
+// per-unit arenas of a cache (unit fork)
+struct ForkArenas {
+  struct Arena { unsigned char* base; int64_t unit_bytes; };
+  Arena a[24];
+  int n;
 };
 
 // ---- launchers ------------------------------------------------------------------------
@@ -241,6 +250,7 @@ template <typename T> cudaError_t launch_window_put(const DevCache&, const T*, c
 template <typename T> cudaError_t launch_refresh(const DevCache&, int, int, int, cudaStream_t);
 template <typename T> cudaError_t launch_attn(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
 cudaError_t launch_dequant(const DevCache&, int, int64_t, int64_t, double*, double*, cudaStream_t);
+cudaError_t launch_fork(const ForkArenas&, int, const int*, const int*, cudaStream_t);
 cudaError_t launch_codes(const DevCache&, int, int64_t, int64_t, uint8_t*, uint8_t*, cudaStream_t);
 cudaError_t launch_quantize_groups(const double*, const int64_t*, int, int, double*, double*, uint8_t*, cudaStream_t);
 cudaError_t launch_pack(const uint8_t*, int64_t, int, uint8_t*, cudaStream_t);

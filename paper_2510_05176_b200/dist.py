@@ -45,6 +45,11 @@ def shard_units(batch: int, layers: int, kv_heads: int, world: int, rank: int, b
     raise ValueError(f"unknown sharding {by!r}")
 
 
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo moves only host tensors: device tensors are staged through host memory."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def gather_head_outputs(local: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather head-sharded attention outputs.
 
@@ -53,12 +58,16 @@ def gather_head_outputs(local: torch.Tensor, group=None) -> torch.Tensor:
     world = dist.get_world_size(group)
     if world == 1:
         return local
+    dev = local.device
     local = local.contiguous()
+    if _host_staged(local, group):
+        local = local.cpu()
     parts = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
     if local.is_cuda:
         dist.all_gather_into_tensor(parts, local, group=group)
     else:
         dist.all_gather(list(parts.unbind(0)), local, group=group)
+    parts = parts.to(dev)
     # [world, B, L, h, G, d] -> [B, L, world*h, G, d]
     return parts.permute(1, 2, 0, 3, 4, 5).reshape(local.shape[0], local.shape[1], -1, *local.shape[3:])
 
@@ -84,10 +93,35 @@ def gather_and_merge_partials(o: torch.Tensor, m: torch.Tensor, l: torch.Tensor,
     if world == 1:
         return lse_merge(o[None], m[None], l[None])
     packed = torch.cat([o.reshape(-1), m.reshape(-1), l.reshape(-1)])
+    dev = packed.device
+    if _host_staged(packed, group):
+        packed = packed.cpu()
     parts = [torch.empty_like(packed) for _ in range(world)]
     dist.all_gather(parts, packed, group=group)
+    parts = [p.to(dev) for p in parts]
     no, nm = o.numel(), m.numel()
     os_ = torch.stack([p[:no].view_as(o) for p in parts])
     ms = torch.stack([p[no:no + nm].view_as(m) for p in parts])
     ls = torch.stack([p[no + nm:].view_as(l) for p in parts])
     return lse_merge(os_, ms, ls)
+
+
+def sequence_block_range(n_blocks: int, world: int, rank: int) -> tuple[int, int, bool]:
+    """Committed-block range [b0, b1) a rank attends in a sequence split, and whether it also
+    takes the exact window (the last rank: it holds the newest tokens)."""
+    b0, b1 = shard_range(n_blocks, world, rank)
+    return b0, b1, rank == world - 1
+
+
+def sequence_split_attention(cache, q: torch.Tensor, group=None, sm_scale: float | None = None) -> torch.Tensor:
+    """Decode attention with the committed tokens of every unit split across the ranks of
+    `group` (cfg3 at 8 GPUs: 4 KV heads cannot occupy 8 GPUs by head sharding alone).  Each
+    rank runs pkv_decode_attn_partial over its block range, the ranks exchange (o, m, l) once
+    and LSE-merge locally.  Returns the normalised [U, G, D] output on every rank."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    b0, b1, win = sequence_block_range(cache.info().n_blocks, world, rank)
+    o, m, l = cache.decode_attention_partial(q, b0, b1, with_window=win, sm_scale=sm_scale)
+    if world == 1:
+        return lse_merge(o[None], m[None], l[None])
+    return gather_and_merge_partials(o, m, l, group=group)
