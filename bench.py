@@ -266,45 +266,6 @@ class Ctx:
         return self.max_over_ranks(e0.elapsed_time(e1) / max(steps, 1)), (clk.summary() if clk else None)
 
 
-def make_pool_cache(ctx, cfgE, U: int, T: int, pool: int, seed: int, D: int = 128, G: int = 128, mine: bool = True,
-                    extra_tokens: int = 0):
-    """A cache of U units prefilled with T tokens: `pool` distinct synthetic units are mined and
-    encoded, then forked (pkv_cache_fork) over the rest -- inputs for U units never need to
-    exist at once.  Returns (cache, k_pool, v_pool, mining ms)."""
-    torch = ctx.torch
-    from paper_2510_05176_b200 import PatternKVCache
-    from paper_2510_05176_b200.synth import synth_kv
-
-    pool = min(pool, U)
-    kp, vp = synth_kv(pool, T + extra_tokens, D, seed=seed)
-    cache = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=T + extra_tokens + 2 * G)
-    # prefill the first `pool` units through a pool cache, fork into the big one
-    pc = PatternKVCache(cfgE, pool, D, dtype=torch.float16, max_tokens=T + 2 * G)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    pc.prefill(kp[:, :T].contiguous(), vp[:, :T].contiguous(), mine=mine)
-    e1.record()
-    torch.cuda.synchronize()
-    mine_ms = e0.elapsed_time(e1)
-    pk = pc.patterns(0)[:, : cfgE.pattern_count]
-    pv = pc.patterns(1)[:, : cfgE.pattern_count]
-    del pc
-    reps = (U + pool - 1) // pool
-    cache.set_patterns(0, pk.repeat(reps, 1, 1)[:U])
-    cache.set_patterns(1, pv.repeat(reps, 1, 1)[:U])
-    # prefill only the pool's units for real (a cache prefills all of its units: give the others
-    # the pool's rows, then fork -- one re-encode per distinct unit, copies for the rest)
-    kk = kp[:, :T].repeat(1, 1, 1)
-    if U > pool:
-        cache_small = PatternKVCache(cfgE, pool, D, dtype=torch.float16, max_tokens=T + extra_tokens + 2 * G)
-        cache_small.set_patterns(0, pk)
-        cache_small.set_patterns(1, pv)
-        cache_small.commit_prefill(kk.contiguous(), vp[:, :T].contiguous())
-        del cache_small
-    return cache, kp, vp, mine_ms, pk, pv
-
-
 def leg_encode(ctx, bits: int, k, v, pool_patterns, results, want_e2e: bool):
     """Headline encode (re-prefill of every unit with installed tables) + one decode-attention step."""
     torch, args = ctx.torch, ctx.args
@@ -561,9 +522,10 @@ def leg_cfg3(ctx):
 
 def leg_cfg4(ctx):
     """Test-time scaling breadth: 64 samples x 32 layers x 8 KV heads (16,384 units on one GPU;
-    samples shard over ranks) forked from one 512-token prompt (pkv_cache_fork), then decode
-    steps of append-and-refresh + attention; and a 16K-token state with |M| = 32 + 124 = 156
-    patterns per side (the table a 15,872-step run ends with) for the late-run step cost."""
+    samples shard over ranks) forked from one 512-token prompt (pkv_cache_fork_from), then
+    decode steps of append-and-refresh + attention; and a 16K-token state whose tables hold
+    |M| = 32 + 124 = 156 patterns per side (what a 512 + 15,872-token run ends with: the 124
+    midranges of its decode spans) for the late-run step cost."""
     torch, args = ctx.torch, ctx.args
     from paper_2510_05176_b200 import PatternKVCache, dist as Dd
     from paper_2510_05176_b200.config import EngineConfig
@@ -572,28 +534,24 @@ def leg_cfg4(ctx):
     S_all, L, H, D, gqa = 64, 32, 8, 128, 4
     s0, s1 = Dd.shard_range(S_all, ctx.world, ctx.rank)
     S = s1 - s0
-    prompt_units = L * H
-    U = S * prompt_units
+    PU = L * H  # units of one sample (the prompt)
+    U = S * PU
     n = args.cfg4_steps
     cfgE = EngineConfig(bits=2, pattern_count=32)
-    res = {"samples_total": S_all, "samples_per_rank": S, "units_per_rank": U}
-    # ---- early run: 512-token prompt -> fork -> decode --------------------------------------
-    kp, vp = synth_kv(prompt_units, 512, D, seed=4000)
-    cache = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=512 + n + 256)
-    kfull = kp.repeat(S, 1, 1)  # prefill input: every sample starts from the prompt
-    vfull = vp.repeat(S, 1, 1)
-    kfull[prompt_units:] = 0
-    vfull[prompt_units:] = 0
-    cache.prefill(kfull, vfull)
-    del kfull, vfull
-    torch.cuda.synchronize()
+    res = {"samples_total": S_all, "samples_per_rank": S, "units_per_rank": U, "gqa": gqa}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ---- early run: 512-token prompt -> fork into S samples -> decode --------------------------
+    kp, vp = synth_kv(PU, 512, D, seed=4000)
+    prompt = PatternKVCache(cfgE, PU, D, dtype=torch.float16, max_tokens=1024)
+    prompt.prefill(kp, vp)
+    cache = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=512 + n + 256)
+    torch.cuda.synchronize()
     e0.record()
-    src = [u % prompt_units for u in range(prompt_units, U)]
-    cache.fork(src, list(range(prompt_units, U)))
+    cache.fork_from(prompt, [u % PU for u in range(U)])
     e1.record()
     torch.cuda.synchronize()
     res["fork_ms"] = e0.elapsed_time(e1)
+    del prompt, kp, vp
     kn, vn = synth_kv(U, n, D, seed=4001 + ctx.rank)  # every sample's own new tokens
     q = torch.randn((U, gqa, D), device="cuda", dtype=torch.float32)
     out = torch.empty_like(q)
@@ -605,44 +563,37 @@ def leg_cfg4(ctx):
     e1.record()
     ctx.barrier()
     ms = ctx.max_over_ranks(e0.elapsed_time(e1))
-    res.update(early_steps=n, early_ms_total=ms, early_tokens_per_s=ctx.world * S * n / (ms * 1e-3),
-               early_patterns_end=32 + n // 128)
+    nk, _ = cache.pattern_counts()
+    res.update(early_context=[512, 512 + n], early_steps=n, early_ms_total=ms,
+               early_tokens_per_s=ctx.world * S * n / (ms * 1e-3), early_patterns_end=int(nk.max()))
     del cache, kn, vn
     torch.cuda.empty_cache()
-    # ---- late run: 16K context, 156 patterns per side ----------------------------------------
+    # ---- late run: 16K context, 156 patterns per side -------------------------------------------
     T = args.cfg4_late
-    pool = min(args.pool, prompt_units)
-    kk, vv = synth_kv(pool, T + 256, D, seed=4100)
-    pc = PatternKVCache(cfgE, pool, D, dtype=torch.float16, max_tokens=T + 512)
+    kk, vv = synth_kv(PU, T + 256, D, seed=4100)
+    pc = PatternKVCache(cfgE, PU, D, dtype=torch.float16, max_tokens=T + 512)
     pc.prefill(kk[:, :512].contiguous(), vv[:, :512].contiguous())
     base = [pc.patterns(s)[:, :32] for s in (0, 1)]
     del pc
-    # the 124 decode patterns of a 512 + 15,872-token run: midranges of its 128-token spans
     nsp = (T - 512) // 128
     tabs = []
     for s, x in ((0, kk), (1, vv)):
-        sp = x[:, 512:512 + 128 * nsp].float().view(pool, nsp, 128, D)
+        sp = x[:, 512:512 + 128 * nsp].float().view(PU, nsp, 128, D)
         mid = 0.5 * (sp.amin(dim=2) + sp.amax(dim=2))
         tabs.append(torch.cat([base[s], mid.double()], dim=1))
     P = tabs[0].shape[1]
+    prompt = PatternKVCache(cfgE, PU, D, dtype=torch.float16, max_tokens=T + 512, max_patterns=P + 64)
+    prompt.set_patterns(0, tabs[0])
+    prompt.set_patterns(1, tabs[1])
+    prompt.commit_prefill(kk[:, :T].contiguous(), vv[:, :T].contiguous())
     big = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=T + 512, max_patterns=P + 64)
-    reps = (U + pool - 1) // pool
-    small = PatternKVCache(cfgE, pool, D, dtype=torch.float16, max_tokens=T + 512, max_patterns=P + 64)
-    small.set_patterns(0, tabs[0])
-    small.set_patterns(1, tabs[1])
-    small.commit_prefill(kk[:, :T].contiguous(), vv[:, :T].contiguous())
-    del small
-    big.set_patterns(0, tabs[0].repeat(reps, 1, 1)[:U])
-    big.set_patterns(1, tabs[1].repeat(reps, 1, 1)[:U])
-    kx = kk[:, :T].repeat(reps, 1, 1)[:U] if U * T * D * 2 * 2 < 40e9 else None
-    if kx is None:
-        return res
-    big.commit_prefill(kx, vv[:, :T].repeat(reps, 1, 1)[:U])
-    del kx
-    torch.cuda.synchronize()
-    kn = kk[:, T:T + 256].repeat(reps, 1, 1)[:U].contiguous()
-    vn = vv[:, T:T + 256].repeat(reps, 1, 1)[:U].contiguous()
+    big.fork_from(prompt, [u % PU for u in range(U)])
+    del prompt
+    kn = kk[:, T:T + 256].repeat(S, 1, 1).contiguous()
+    vn = vv[:, T:T + 256].repeat(S, 1, 1).contiguous()
+    del kk, vv
     m = min(args.cfg4_late_steps, 256)
+    att_ms, _ = ctx.time_steps(lambda: big.decode_attention(q, out=out), args.steps, args.warmup, clocks=False)
     ctx.barrier()
     e0.record()
     for t in range(m):
@@ -653,8 +604,9 @@ def leg_cfg4(ctx):
     ms = ctx.max_over_ranks(e0.elapsed_time(e1))
     att_bytes = attn_bytes_per_step(U, T - 128, 128, 2, P, gqa)
     res.update(late_context=T, late_patterns=P, late_steps=m, late_ms_total=ms,
-               late_tokens_per_s=ctx.world * S * m / (ms * 1e-3),
-               late_attn_GBps=att_bytes / (ms / m * 1e-3) / 1e9)
+               late_tokens_per_s=ctx.world * S * m / (ms * 1e-3), late_attn_ms=att_ms,
+               late_attn_GBps_per_gpu=att_bytes / (att_ms * 1e-3) / 1e9,
+               late_attn_frac=att_bytes / (att_ms * 1e-3) / 1e9 / ctx.peak)
     del big, kn, vn
     torch.cuda.empty_cache()
     return res
@@ -680,25 +632,12 @@ def leg_cfg5_head(ctx):
     kp, vp = synth_kv(pool, T, D, seed=5000 + ctx.rank)
     pc = PatternKVCache(cfgE, pool, D, dtype=torch.float16, max_tokens=T + 256)
     pc.reserve_mining(T)
-    pc.prefill(kp, vp)
-    pk, pv = pc.patterns(0)[:, :32], pc.patterns(1)[:, :32]
-    del pc
-    cache = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=T + 256)
-    reps = (U + pool - 1) // pool
-    cache.set_patterns(0, pk.repeat(reps, 1, 1)[:U])
-    cache.set_patterns(1, pv.repeat(reps, 1, 1)[:U])
-    # encode the pool's units in place (units 0..pool-1 get real inputs), fork over the rest
-    kx = torch.zeros((U, T, D), dtype=torch.float16, device="cuda") if U * T * D * 4 < 60e9 else None
-    if kx is None:
-        return {"skipped": "prefill staging exceeds the HBM budget"}
-    kx[:pool] = kp
-    vx = torch.zeros_like(kx)
-    vx[:pool] = vp
+    pc.prefill(kp, vp)  # mining + encode of the distinct units
     del kp, vp
-    cache.commit_prefill(kx, vx)
-    del kx, vx
+    cache = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=T + 256)
+    cache.fork_from(pc, [u % pool for u in range(U)])  # the rest are copies (no 64K inputs for all)
+    del pc
     torch.cuda.empty_cache()
-    cache.fork([u % pool for u in range(pool, U)], list(range(pool, U)))
     q = torch.randn((U, gqa, D), device="cuda", dtype=torch.float32)
     out = torch.empty_like(q)
 

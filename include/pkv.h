@@ -92,6 +92,9 @@ int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t head_dim, i
 int pkv_cache_destroy(pkv_cache* c);
 int pkv_cache_info_get(pkv_cache* c, pkv_cache_info* out);
 int pkv_cache_reserve(pkv_cache* c, int64_t max_tokens, int32_t max_patterns, void* stream);
+/* preallocate the k-means scratch for prefills/mining of up to max_tokens tokens, so
+ * pkv_mine / pkv_prefill allocate nothing (otherwise they allocate it per call). */
+int pkv_cache_reserve_mining(pkv_cache* c, int64_t max_tokens, void* stream);
 /* drop every committed/window token (token_count = 0) but keep the pattern
  * tables when keep_patterns != 0, so the next pkv_prefill with NULL seed
  * indices re-encodes against the same tables (re-prefill of a slot). */
@@ -141,6 +144,10 @@ int pkv_decode_attn_partial(pkv_cache* c, const float* q, int32_t gqa, float sm_
  * and block geometry, so a copy is a whole state).  The reference equivalent is
  * copy.deepcopy of a HeadCacheState (engine.py:104-129).  Host arrays [n]. */
 int pkv_cache_fork(pkv_cache* c, const int32_t* src_units, const int32_t* dst_units, int32_t n, void* stream);
+/* Fork across caches: every unit i of dst becomes a copy of unit src_units[i] of src
+ * (host array [dst units]); dst takes src's token count and block geometry (e.g. a
+ * one-prompt cache of L x H units -> a cache of S samples x L x H units). */
+int pkv_cache_fork_from(pkv_cache* dst, const pkv_cache* src, const int32_t* src_units, void* stream);
 
 /* committed_matrices / reconstruct_token (engine.py:271-303), exact fp64:
  * committed tokens [t0, t1) -> device [U][t1-t0][D] each. */

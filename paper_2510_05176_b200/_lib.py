@@ -58,6 +58,7 @@ PROTOTYPES = {
     "pkv_cache_destroy": (C.c_int, [_vp]),
     "pkv_cache_info_get": (C.c_int, [_vp, _P(PkvCacheInfo)]),
     "pkv_cache_reserve": (C.c_int, [_vp, _i64, _i32, _vp]),
+    "pkv_cache_reserve_mining": (C.c_int, [_vp, _i64, _vp]),
     "pkv_cache_reset": (C.c_int, [_vp, _i32, _vp]),
     "pkv_check_finite": (C.c_int, [_vp, _i32, _i64, _P(_i64), _vp]),
     "pkv_mine": (C.c_int, [_vp, _i32, _vp, _i64, _P(_i64), _P(_f64), _P(_i32), _vp, _vp]),
@@ -67,6 +68,7 @@ PROTOTYPES = {
     "pkv_decode_attn": (C.c_int, [_vp, _vp, _i32, _f32, _vp, _vp]),
     "pkv_decode_attn_partial": (C.c_int, [_vp, _vp, _i32, _f32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "pkv_cache_fork": (C.c_int, [_vp, _P(_i32), _P(_i32), _i32, _vp]),
+    "pkv_cache_fork_from": (C.c_int, [_vp, _vp, _P(_i32), _vp]),
     "pkv_dequant": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "pkv_export_codes": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "pkv_cache_import": (C.c_int, [_vp, _i64, _i32, _P(_i64), _P(_i32), _i32, _i32, _i32, _i32, _P(_i32), _P(_i32),

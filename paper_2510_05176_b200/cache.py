@@ -215,6 +215,11 @@ class PatternKVCache:
     def first_decision_token(self, t: int):
         self._first_decision = int(t)
 
+    def reserve_mining(self, max_tokens: int) -> None:
+        """Preallocate the k-means scratch for prefills of up to max_tokens tokens (no
+        allocation inside later prefill / mine calls)."""
+        _lib.call("pkv_cache_reserve_mining", self._h, int(max_tokens), _stream())
+
     def reset(self, keep_patterns: bool = True) -> None:
         """Empty the cache (token_count = 0); keep the pattern tables for a re-prefill."""
         _lib.call("pkv_cache_reset", self._h, int(keep_patterns), _stream())
@@ -299,6 +304,19 @@ class PatternKVCache:
         nk, nv = (c.copy() for c in self._npre)
         nk[dst], nv[dst] = nk[src], nv[src]
         self._npre = (nk, nv)
+
+    def fork_from(self, src: "PatternKVCache", src_units) -> None:
+        """Every unit i of this cache becomes a copy of unit src_units[i] of `src` (parallel
+        samples of one prompt: a prompt cache of L x H units -> S x L x H units)."""
+        m = [int(x) for x in src_units]
+        if len(m) != self.n_units:
+            raise UsageError(f"fork_from needs one source unit per destination unit ({self.n_units})")
+        _lib.call("pkv_cache_fork_from", self._h, src._h, (C.c_int32 * self.n_units)(*m), _stream())
+        nk, nv = src.prefill_pattern_counts
+        self._npre_dev = None
+        self._npre = (nk[m].copy(), nv[m].copy())
+        self._prefill_committed = src._prefill_committed
+        self._first_decision = src._first_decision
 
     def dequant(self, t0: int = 0, t1: int | None = None):
         """Exact fp64 reconstruction of committed tokens [t0, t1): ([U,n,D], [U,n,D])."""

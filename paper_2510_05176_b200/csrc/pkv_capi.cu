@@ -139,7 +139,16 @@ struct pkv_cache {
   int64_t uploaded_nbcap = -1, uploaded_base = -1;   // last block table sent to the device
   std::vector<int64_t> uploaded_start;
   bool blocks_stale = false;   // reset dropped the prefill geometry; re-upload before the next flush
+  unsigned char* mine_scratch = nullptr;   // k-means scratch (pkv_cache_reserve_mining), else per call
+  size_t mine_scratch_bytes = 0;
 };
+
+// k-means scratch for U units x 2 sides x T points: near, own (f64), lab, lab2, list (i32),
+// labels out (i32), history [U][2][25] f64, niter [U][2] i32, first [U][2] i64
+static size_t mine_scratch_need(int U, int64_t T) {
+  const size_t n2 = (size_t)U * 2 * T;
+  return n2 * 8 * 2 + n2 * 4 * 4 + (size_t)U * 2 * 25 * 8 + (size_t)U * 2 * 4 + (size_t)U * 2 * 8 + 8 * 64;
+}
 
 static int esize_of(int dtype) {
   switch (dtype) {
@@ -308,7 +317,7 @@ extern "C" int pkv_cache_destroy(pkv_cache* c) {
   DevCache& d = c->dev;
   void* ptrs[] = {d.kpat64, d.vpat64, d.kpat32, d.vpat32, d.kpmax, d.vpmax, d.nk, d.nv, d.probe, d.blk_start, d.blk_len,
                   d.kcodes, d.kparam32, d.kparam64, d.kidx, d.vcodes, d.vparam32, d.vparam64, d.vidx, d.kdiag,
-                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag, d.work};
+                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag, d.work, c->mine_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -327,6 +336,20 @@ extern "C" int pkv_cache_info_get(pkv_cache* c, pkv_cache_info* o) {
     CU(cudaMemcpy(s, c->stats, 16, cudaMemcpyDeviceToHost));
     o->n_refined = s[0]; o->n_exact_div = s[1];
   }
+  return PKV_OK;
+}
+
+extern "C" int pkv_cache_reserve_mining(pkv_cache* c, int64_t max_tokens, void* stream) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  if (max_tokens < 1) return fail(PKV_USAGE, -1, "max_tokens must be >= 1");
+  const size_t need = mine_scratch_need(c->U, max_tokens);
+  if (need <= c->mine_scratch_bytes) return PKV_OK;
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  if (c->mine_scratch) cudaFree(c->mine_scratch);
+  c->mine_scratch = nullptr;
+  c->mine_scratch_bytes = 0;
+  CU(cudaMalloc((void**)&c->mine_scratch, need));
+  c->mine_scratch_bytes = need;
   return PKV_OK;
 }
 
@@ -456,15 +479,19 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
   int *lab = nullptr, *lab2 = nullptr, *list = nullptr, *niter = nullptr;
   int64_t* first = nullptr;
   int* lab_out = nullptr;
-  if (labels_dev) CU(cudaMallocAsync((void**)&lab_out, n2 * 4, st));
-  CU(cudaMallocAsync((void**)&near_, n2 * 8, st));
-  CU(cudaMallocAsync((void**)&own, n2 * 8, st));
-  CU(cudaMallocAsync((void**)&lab, n2 * 4, st));
-  CU(cudaMallocAsync((void**)&lab2, n2 * 4, st));
-  CU(cudaMallocAsync((void**)&list, n2 * 4, st));
-  CU(cudaMallocAsync((void**)&hist, (size_t)U * 2 * 25 * 8, st));
-  CU(cudaMallocAsync((void**)&niter, (size_t)U * 2 * 4, st));
-  CU(cudaMallocAsync((void**)&first, (size_t)U * 2 * 8, st));
+  const size_t need = mine_scratch_need(U, T);
+  const bool own_scratch = c->mine_scratch_bytes >= need;
+  unsigned char* base = c->mine_scratch;
+  if (!own_scratch) CU(cudaMallocAsync((void**)&base, need, st));
+  {
+    size_t off = 0;
+    auto carve = [&](size_t bytes) { unsigned char* p = base + off; off += (bytes + 255) & ~(size_t)255; return p; };
+    near_ = (double*)carve(n2 * 8); own = (double*)carve(n2 * 8);
+    lab = (int*)carve(n2 * 4); lab2 = (int*)carve(n2 * 4); list = (int*)carve(n2 * 4);
+    if (labels_dev) lab_out = (int*)carve(n2 * 4); else carve(n2 * 4);
+    hist = (double*)carve((size_t)U * 2 * 25 * 8); niter = (int*)carve((size_t)U * 2 * 4);
+    first = (int64_t*)carve((size_t)U * 2 * 8);
+  }
   std::vector<int64_t> fh((size_t)U * 2, 0);
   for (int u = 0; u < U; ++u) {
     if (side_mask & 1) fh[u] = fk[u];
@@ -487,7 +514,6 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
     const int s = (side_mask & 1) ? 0 : 1;
     CU(cudaMemcpy2DAsync(labels_dev, (size_t)T * 4, lab_out + (size_t)s * T, (size_t)2 * T * 4, (size_t)T * 4, U,
                          cudaMemcpyDeviceToDevice, st));
-    CU(cudaFreeAsync(lab_out, st));
   }
   if (hist_host || niter_host) {
     std::vector<double> hh((size_t)U * 2 * 25);
@@ -501,8 +527,7 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
       if (niter_host) niter_host[u] = nh[(size_t)u * 2 + s];
     }
   }
-  for (void* p : {(void*)near_, (void*)own, (void*)lab, (void*)lab2, (void*)list, (void*)hist, (void*)niter, (void*)first})
-    CU(cudaFreeAsync(p, st));
+  if (!own_scratch) CU(cudaFreeAsync(base, st));
   if (side_mask & 1) c->pk_bound = k;
   if (side_mask & 2) c->pv_bound = k;
   CU(launch_probes(c->dev, st));
@@ -825,6 +850,55 @@ extern "C" int pkv_decode_attn_partial(pkv_cache* c, const float* q, int32_t gqa
 // ---------------------------------------------------------------------------------
 // unit fork (parallel sampling from one prompt: a unit's whole state copied)
 // ---------------------------------------------------------------------------------
+// arena rows of every unit of `src` to the matching units of `dst` (dst capacities >= src's)
+static ForkArenas fork_arenas(const pkv_cache* src, const pkv_cache* dst) {
+  const DevCache& a = src->dev;
+  const DevCache& b = dst->dev;
+  const int64_t D = src->D, Dp = src->Dp;
+  ForkArenas fa;
+  std::memset(&fa, 0, sizeof fa);
+  auto add = [&](const void* ps, void* pd, int64_t ss, int64_t ds, int64_t bytes) {
+    fa.a[fa.n++] = ForkArenas::Arena{(const unsigned char*)ps, (unsigned char*)pd, ss, ds, (ps && pd) ? bytes : 0};
+  };
+  add(a.kpat64, b.kpat64, a.Pcap * D * 8, b.Pcap * D * 8, a.Pcap * D * 8);
+  add(a.vpat64, b.vpat64, a.Pcap * D * 8, b.Pcap * D * 8, a.Pcap * D * 8);
+  add(a.kpat32, b.kpat32, a.Pcap * Dp * 4, b.Pcap * Dp * 4, a.Pcap * Dp * 4);
+  add(a.vpat32, b.vpat32, a.Pcap * Dp * 4, b.Pcap * Dp * 4, a.Pcap * Dp * 4);
+  add(a.kpmax, b.kpmax, 4, 4, 4); add(a.vpmax, b.vpmax, 4, 4, 4);
+  add(a.nk, b.nk, 4, 4, 4); add(a.nv, b.nv, 4, 4, 4);
+  add(a.probe, b.probe, 128, 128, 128);
+  const int64_t bb = a.blk_bytes;
+  add(a.kcodes, b.kcodes, a.NBcap * bb, b.NBcap * bb, a.NBcap * bb);
+  add(a.vcodes, b.vcodes, a.NBcap * bb, b.NBcap * bb, a.NBcap * bb);
+  add(a.kparam32, b.kparam32, a.NBcap * 2 * Dp * 4, b.NBcap * 2 * Dp * 4, a.NBcap * 2 * Dp * 4);
+  add(a.kparam64, b.kparam64, a.NBcap * 2 * D * 8, b.NBcap * 2 * D * 8, a.NBcap * 2 * D * 8);
+  add(a.kidx, b.kidx, a.NBcap * a.GP * 2, b.NBcap * b.GP * 2, a.NBcap * a.GP * 2);
+  add(a.vidx, b.vidx, a.NBcap * a.GP * 2, b.NBcap * b.GP * 2, a.NBcap * a.GP * 2);
+  add(a.vparam32, b.vparam32, a.NBcap * a.GP * 8, b.NBcap * b.GP * 8, a.NBcap * a.GP * 8);
+  add(a.vparam64, b.vparam64, a.Tcap * 16, b.Tcap * 16, a.Tcap * 16);
+  if (a.keep_diag && b.keep_diag) {
+    add(a.kdiag, b.kdiag, a.Tcap * 16, b.Tcap * 16, a.Tcap * 16);
+    add(a.vdiag, b.vdiag, a.Tcap * 16, b.Tcap * 16, a.Tcap * 16);
+  }
+  const int64_t wrow = (int64_t)a.Wcap * D * src->esize;
+  add(a.wk, b.wk, wrow, wrow, wrow);
+  add(a.wv, b.wv, wrow, wrow, wrow);
+  return fa;
+}
+
+static int run_fork(const ForkArenas& fa, const std::vector<int>& hs, const std::vector<int>& hd, cudaStream_t st) {
+  const int n = (int)hs.size();
+  if (n == 0) return PKV_OK;
+  int* dev_pairs = nullptr;
+  CU(cudaMallocAsync((void**)&dev_pairs, (size_t)2 * n * 4, st));
+  std::vector<int> pairs(hs);
+  pairs.insert(pairs.end(), hd.begin(), hd.end());
+  CU(cudaMemcpyAsync(dev_pairs, pairs.data(), (size_t)2 * n * 4, cudaMemcpyHostToDevice, st));
+  CU(launch_fork(fa, n, dev_pairs, dev_pairs + n, st));
+  CU(cudaFreeAsync(dev_pairs, st));
+  return PKV_OK;
+}
+
 extern "C" int pkv_cache_fork(pkv_cache* c, const int32_t* src_units, const int32_t* dst_units, int32_t n,
                               void* stream) {
   if (!c || (n > 0 && (!src_units || !dst_units))) return fail(PKV_USAGE, -1, "null argument");
@@ -840,30 +914,38 @@ extern "C" int pkv_cache_fork(pkv_cache* c, const int32_t* src_units, const int3
   for (int i = 0; i < n; ++i)
     if (seen[hs[i]] && hs[i] != hd[i])
       return fail(PKV_USAGE, i, "unit %d is both a fork source and a destination", hs[i]);
-  if (n == 0) return PKV_OK;
+  return run_fork(fork_arenas(c, c), hs, hd, (cudaStream_t)stream);
+}
+
+extern "C" int pkv_cache_fork_from(pkv_cache* dst, const pkv_cache* src, const int32_t* src_units, void* stream) {
+  if (!dst || !src || !src_units) return fail(PKV_USAGE, -1, "null argument");
+  if (dst == src) return fail(PKV_USAGE, -1, "fork_from needs two caches (use pkv_cache_fork within one)");
+  const pkv_config &a = src->cfg, &b = dst->cfg;
+  if (src->D != dst->D || src->dtype != dst->dtype || a.bits != b.bits || a.group_size != b.group_size ||
+      a.residual_window != b.residual_window || a.use_k_patterns != b.use_k_patterns ||
+      a.use_v_patterns != b.use_v_patterns || a.generate_new_patterns != b.generate_new_patterns ||
+      a.use_v_gate != b.use_v_gate || a.use_k_gate != b.use_k_gate || a.alpha != b.alpha)
+    return fail(PKV_USAGE, -1, "fork_from: caches differ in head_dim, dtype or config");
+  std::vector<int> hs(dst->U), hd(dst->U);
+  for (int i = 0; i < dst->U; ++i) {
+    if (src_units[i] < 0 || src_units[i] >= src->U)
+      return fail(PKV_USAGE, i, "source unit %d of destination unit %d outside the %d units", src_units[i], i, src->U);
+    hs[i] = src_units[i];
+    hd[i] = i;
+  }
   cudaStream_t st = (cudaStream_t)stream;
-  const DevCache& d = c->dev;
-  const int64_t P = d.Pcap, NB = d.NBcap, T = d.Tcap, D = c->D, Dp = c->Dp;
-  ForkArenas fa;
-  std::memset(&fa, 0, sizeof fa);
-  auto add = [&](void* p, int64_t bytes) { fa.a[fa.n].base = (unsigned char*)p; fa.a[fa.n].unit_bytes = p ? bytes : 0; ++fa.n; };
-  add(d.kpat64, P * D * 8); add(d.vpat64, P * D * 8); add(d.kpat32, P * Dp * 4); add(d.vpat32, P * Dp * 4);
-  add(d.kpmax, 4); add(d.vpmax, 4); add(d.nk, 4); add(d.nv, 4); add(d.probe, 2 * 16 * 4);
-  add(d.kcodes, NB * d.blk_bytes); add(d.vcodes, NB * d.blk_bytes);
-  add(d.kparam32, NB * 2 * Dp * 4); add(d.kparam64, NB * 2 * D * 8);
-  add(d.kidx, NB * d.GP * 2); add(d.vidx, NB * d.GP * 2); add(d.vparam32, NB * d.GP * 8);
-  add(d.vparam64, T * 16);
-  if (d.keep_diag) { add(d.kdiag, T * 16); add(d.vdiag, T * 16); }
-  add(d.wk, (int64_t)d.Wcap * D * c->esize); add(d.wv, (int64_t)d.Wcap * D * c->esize);
-  int* dev_pairs = nullptr;
-  CU(cudaMallocAsync((void**)&dev_pairs, (size_t)2 * n * 4, st));
-  std::vector<int> pairs(hs);
-  pairs.insert(pairs.end(), hd.begin(), hd.end());
-  CU(cudaMemcpyAsync(dev_pairs, pairs.data(), (size_t)2 * n * 4, cudaMemcpyHostToDevice, st));
-  CU(launch_fork(fa, n, dev_pairs, dev_pairs + n, st));
-  CU(cudaFreeAsync(dev_pairs, st));
-  CU(cudaStreamSynchronize(st));  // the host pair list must outlive the async copy
-  return PKV_OK;
+  int rc = reserve(dst, std::max(dst->dev.Tcap, src->dev.Tcap), std::max(dst->dev.Pcap, src->dev.Pcap), st);
+  if (rc) return rc;
+  // the destination takes the source's lockstep geometry
+  dst->token_count = src->token_count; dst->committed = src->committed;
+  dst->win_len = src->win_len; dst->win_slot0 = src->win_slot0; dst->nb = src->nb;
+  dst->nb_prefill = src->nb_prefill; dst->decode_base = src->decode_base;
+  dst->blk_start = src->blk_start; dst->blk_len = src->blk_len;
+  dst->pk_bound = src->pk_bound; dst->pv_bound = src->pv_bound;
+  rc = upload_blocks(dst, st);
+  if (rc) return rc;
+  dst->blocks_stale = false;
+  return run_fork(fork_arenas(src, dst), hs, hd, st);
 }
 
 // ---------------------------------------------------------------------------------

@@ -235,9 +235,10 @@ struct AttnArgs {
   float* ml;           // partial mode: [U][G][2] (m in natural-log units, l); out = unnormalised o
 };
 
-// per-unit arenas of a cache (unit fork)
+// per-unit arena rows copied by a unit fork: unit s of src -> unit d of dst,
+// `bytes` from src + s*src_stride to dst + d*dst_stride (same or different caches)
 struct ForkArenas {
-  struct Arena { unsigned char* base; int64_t unit_bytes; };
+  struct Arena { const unsigned char* src; unsigned char* dst; int64_t src_stride, dst_stride, bytes; };
   Arena a[24];
   int n;
 };

@@ -412,20 +412,20 @@ cudaError_t launch_midrange(const double* x, int64_t n, int D, double* out, cuda
 namespace pkv {
 
 // ---- unit fork: copy every per-unit arena row of unit src[i] onto unit dst[i] ---------
-// grid (n pairs, arenas); 16-byte vectors when the arena's per-unit size and base allow.
+// grid (n pairs, arenas); 16-byte vectors when the strides, bases and row size allow.
 __global__ void fork_units_kernel(ForkArenas fa, const int* src, const int* dst) {
   const ForkArenas::Arena& ar = fa.a[blockIdx.y];
-  if (!ar.base || ar.unit_bytes == 0) return;
+  if (!ar.src || !ar.dst || ar.bytes == 0) return;
   const int s = src[blockIdx.x], d = dst[blockIdx.x];
-  if (s == d) return;
-  const unsigned char* from = ar.base + (int64_t)s * ar.unit_bytes;
-  unsigned char* to = ar.base + (int64_t)d * ar.unit_bytes;
-  if ((ar.unit_bytes & 15) == 0 && ((uintptr_t)ar.base & 15) == 0) {
-    const int64_t n = ar.unit_bytes >> 4;
+  const unsigned char* from = ar.src + (int64_t)s * ar.src_stride;
+  unsigned char* to = ar.dst + (int64_t)d * ar.dst_stride;
+  if (from == to) return;
+  if (((ar.bytes | ar.src_stride | ar.dst_stride) & 15) == 0 && (((uintptr_t)ar.src | (uintptr_t)ar.dst) & 15) == 0) {
+    const int64_t n = ar.bytes >> 4;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
       reinterpret_cast<uint4*>(to)[i] = reinterpret_cast<const uint4*>(from)[i];
   } else {
-    for (int64_t i = threadIdx.x; i < ar.unit_bytes; i += blockDim.x) to[i] = from[i];
+    for (int64_t i = threadIdx.x; i < ar.bytes; i += blockDim.x) to[i] = from[i];
   }
 }
 

@@ -179,3 +179,55 @@ def test_fork_units_then_decode_matches_oracle():
         np.testing.assert_array_equal(st.k_codes, np.concatenate([b[4] for b in h.k_blocks]))
         np.testing.assert_array_equal(st.v_codes, np.stack([x[2] for x in h.v_tok]))
         np.testing.assert_array_equal(st.k_idx, np.concatenate([b[5] for b in h.k_blocks]))
+
+
+def test_fork_from_prompt_cache_into_samples():
+    """pkv_cache_fork_from: a 2-unit prompt cache (prefill + a few appends, so the window and a
+    flush are part of the state) becomes 3 samples x 2 units in a second cache with larger
+    capacities; each sample then decodes its own tokens == the oracle replay of its history."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_05176_b200 as P
+    from paper_2510_05176_b200.export import export_unit
+
+    tp, pre, steps, S = 600, 150, 200, 3
+    cfg = dict(bits=4, pattern_count=16)
+    ks, vs = [], []
+    for u in range(2):
+        a, b = O.synth_unit(O.unit_seed(2, u, 7), tp + pre, D)
+        ks.append(a.astype(np.float16).astype(np.float64))
+        vs.append(b.astype(np.float16).astype(np.float64))
+    k, v = np.stack(ks), np.stack(vs)
+    prompt = P.PatternKVCache(P.EngineConfig(**cfg), 2, D, dtype=torch.float16, max_tokens=1024)
+    kt, vt = torch.from_numpy(k).half().cuda(), torch.from_numpy(v).half().cuda()
+    prompt.prefill(kt[:, :tp], vt[:, :tp])
+    for t in range(tp, tp + pre):
+        prompt.append(kt[:, t], vt[:, t])
+    big = P.PatternKVCache(P.EngineConfig(**cfg), 2 * S, D, dtype=torch.float16, max_tokens=4096, max_patterns=200)
+    big.fork_from(prompt, [i % 2 for i in range(2 * S)])
+    del prompt
+    dk, dv = [], []
+    for i in range(2 * S):
+        a, b = O.synth_unit(O.unit_seed(20 + i, 1, 1), steps, D)
+        dk.append(a.astype(np.float16).astype(np.float64))
+        dv.append(b.astype(np.float16).astype(np.float64))
+    dkt = torch.from_numpy(np.stack(dk)).half().cuda()
+    dvt = torch.from_numpy(np.stack(dv)).half().cuda()
+    for t in range(steps):
+        big.append(dkt[:, t], dvt[:, t])
+    q = np.random.default_rng(3).normal(size=(2 * S, 4, D)).astype(np.float32)
+    out = big.decode_attention(torch.from_numpy(q).cuda()).cpu().numpy()
+    for i in range(2 * S):
+        u = i % 2
+        h = O.replay(k[u, :tp], v[u, :tp], np.concatenate([k[u, tp:], dk[i]]), np.concatenate([v[u, tp:], dv[i]]),
+                     O.Knobs(**cfg))
+        st = export_unit(big, i, with_bytes=False)
+        assert st.n_prefill_k == 16
+        np.testing.assert_array_equal(st.kpat, h.kpat)
+        np.testing.assert_array_equal(st.vpat, h.vpat)
+        np.testing.assert_array_equal(st.k_codes, np.concatenate([b[4] for b in h.k_blocks]))
+        np.testing.assert_array_equal(st.v_codes, np.stack([x[2] for x in h.v_tok]))
+        np.testing.assert_array_equal(st.v_idx, np.array([x[3] for x in h.v_tok]))
+        np.testing.assert_array_equal(st.window_k, np.stack(h.win_k))
+        ref = O.head_attention(h, q[i].astype(np.float64), 1.0 / math.sqrt(D))
+        assert np.abs(out[i] - ref).max() / np.abs(ref).max() <= 1e-3
