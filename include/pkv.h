@@ -100,8 +100,19 @@ int pkv_cache_reserve_mining(pkv_cache* c, int64_t max_tokens, void* stream);
  * indices re-encodes against the same tables (re-prefill of a slot). */
 int pkv_cache_reset(pkv_cache* c, int32_t keep_patterns, void* stream);
 
-/* engine.py:132-139 / :180-181 finiteness checks: *first_bad = flat index of the
- * first non-finite element or -1.  Synchronous on `stream`. */
+/* Fused finiteness checks (engine.py:132-139 / :180-181): the kernels that read caller
+ * K/V (K1-TC's tensor-core scores, K1's staging, the window copy) record the first
+ * non-finite element (lowest unit, K before V, token, dim) in the cache; pkv_prefill /
+ * pkv_append publish it to pinned host memory without synchronising.  pkv_cache_check
+ * returns PKV_DATA with the reference's message ("non-finite prefill K element at token
+ * t, dim j" / "non-finite decode vector at token t", plus the unit) once the flagged work
+ * has run -- wait != 0 blocks until the last prefill/append has; where (optional) [4] =
+ * unit, side, token, dim.  pkv_append refuses a flagged cache; pkv_cache_reset and
+ * pkv_prefill clear the flag.  A flagged cache's contents are unspecified. */
+int pkv_cache_check(pkv_cache* c, int32_t wait, int64_t* where);
+
+/* standalone finiteness scan: *first_bad = flat index of the first non-finite element
+ * or -1.  Synchronous on `stream`. */
 int pkv_check_finite(const void* x, int32_t dtype, int64_t n, int64_t* first_bad, void* stream);
 
 /* mine_patterns (patterns.py:145-158) for every unit of one side (0 = K, 1 = V).

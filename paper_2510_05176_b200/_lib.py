@@ -61,6 +61,7 @@ PROTOTYPES = {
     "pkv_cache_reserve_mining": (C.c_int, [_vp, _i64, _vp]),
     "pkv_cache_reset": (C.c_int, [_vp, _i32, _vp]),
     "pkv_check_finite": (C.c_int, [_vp, _i32, _i64, _P(_i64), _vp]),
+    "pkv_cache_check": (C.c_int, [_vp, _i32, _P(_i64)]),
     "pkv_mine": (C.c_int, [_vp, _i32, _vp, _i64, _P(_i64), _P(_f64), _P(_i32), _vp, _vp]),
     "pkv_set_patterns": (C.c_int, [_vp, _i32, _vp, _i32, _vp]),
     "pkv_prefill": (C.c_int, [_vp, _vp, _vp, _i64, _P(_i64), _P(_i64), _vp]),

@@ -156,19 +156,17 @@ class PatternKVCache:
         return bad.value
 
     # ---- lifecycle ------------------------------------------------------------------
-    def prefill(self, k: torch.Tensor, v: torch.Tensor, mine: bool = True, validate: bool = False) -> None:
-        """engine.py:142-169 for every unit: k, v [U, T, D]."""
+    def prefill(self, k: torch.Tensor, v: torch.Tensor, mine: bool = True, sync_check: bool = False) -> None:
+        """engine.py:142-169 for every unit: k, v [U, T, D].
+
+        Non-finite inputs are detected inside the kernels (no extra pass, no host sync) and
+        raised as DataError by the next call that checks -- ``check()``, ``append`` -- once
+        the GPU has run this prefill; ``sync_check=True`` waits for it and raises here."""
         k = self._as_input(k, 3, "prefill K")
         v = self._as_input(v, 3, "prefill V")
         if k.shape != v.shape:
             raise UsageError(f"prefill K {tuple(k.shape)} and V {tuple(v.shape)} must have equal shapes")
         T = k.shape[1]
-        if validate:
-            for name, x in (("K", k), ("V", v)):
-                bad = self.check_finite(x)
-                if bad >= 0:
-                    t, j = (bad // self.head_dim) % T, bad % self.head_dim
-                    raise DataError(f"non-finite prefill {name} element at token {t}, dim {j}")
         cfg = self.config
         fk = fv = None
         if mine and cfg.use_k_patterns:
@@ -180,6 +178,14 @@ class PatternKVCache:
         self._npre_dev = (self.read("nk", torch.int32, (self.n_units,)), self.read("nv", torch.int32, (self.n_units,)))
         self._prefill_committed = T - min(T, cfg.residual_window)
         self._first_decision = None
+        if sync_check:
+            self.check(wait=True)
+
+    def check(self, wait: bool = True) -> None:
+        """Raise DataError (the reference's message + unit) if a prefill / append fed a
+        non-finite element (engine.py:136-138, 180-181); wait=False only looks at work the
+        GPU has already finished."""
+        _lib.call("pkv_cache_check", self._h, int(bool(wait)), None)
 
     # ---- prefill bookkeeping (read lazily) ------------------------------------------------
     @property
@@ -235,13 +241,14 @@ class PatternKVCache:
         """Prefill with the installed pattern tables (no mining)."""
         self.prefill(k, v, mine=False)
 
-    def append(self, k: torch.Tensor, v: torch.Tensor, validate: bool = False) -> None:
-        """engine.py:172-198 for every unit: k, v [U, D]."""
+    def append(self, k: torch.Tensor, v: torch.Tensor, sync_check: bool = False) -> None:
+        """engine.py:172-198 for every unit: k, v [U, D].  A non-finite row is flagged inside
+        the window copy and raised by a later check()/append (or here with sync_check=True)."""
         k = self._as_input(k, 2, "decode K")
         v = self._as_input(v, 2, "decode V")
-        if validate and (self.check_finite(k) >= 0 or self.check_finite(v) >= 0):
-            raise DataError(f"non-finite decode vector at token {self.info().token_count}")
         _lib.call("pkv_append", self._h, _ptr(k), _ptr(v), _stream())
+        if sync_check:
+            self.check(wait=True)
 
     def mine(self, side: int, x: torch.Tensor, seed: int, labels: bool = False):
         """mine_patterns for every unit (patterns.py:145-158); returns (history [U, 25], niter [U])

@@ -141,6 +141,11 @@ struct pkv_cache {
   bool blocks_stale = false;   // reset dropped the prefill geometry; re-upload before the next flush
   unsigned char* mine_scratch = nullptr;   // k-means scratch (pkv_cache_reserve_mining), else per call
   size_t mine_scratch_bytes = 0;
+  // fused non-finite detection: the kernels atomicMin dev.bad; every prefill / append copies it
+  // into pinned host memory behind an event, so the host reads it without a stream sync
+  unsigned long long* bad_host = nullptr;
+  cudaEvent_t bad_ev = nullptr;
+  int64_t prefill_tokens = 0;  // tokens of the last prefill (keys below are prefill rows)
 };
 
 // k-means scratch for U units x 2 sides x T points: near, own (f64), lab, lab2, list (i32),
@@ -205,6 +210,29 @@ static int upload_blocks(pkv_cache* c, cudaStream_t st) {
   c->uploaded_start = c->blk_start;
   c->uploaded_base = c->decode_base;
   return PKV_OK;
+}
+
+// publish the device non-finite flag to pinned host memory (stream ordered, no sync)
+static int publish_bad(pkv_cache* c, cudaStream_t st) {
+  CU(cudaMemcpyAsync(c->bad_host, c->dev.bad, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaEventRecord(c->bad_ev, st));
+  return PKV_OK;
+}
+
+// PKV_DATA with the reference's message when a finished prefill / append saw a non-finite
+// input; wait = block until the last published flag is on the host
+static int check_bad(pkv_cache* c, int wait, int64_t* where) {
+  if (wait) CU(cudaEventSynchronize(c->bad_ev));
+  else if (cudaEventQuery(c->bad_ev) != cudaSuccess) { (void)cudaGetLastError(); return PKV_OK; }
+  const unsigned long long key = *(volatile unsigned long long*)c->bad_host;
+  if (key == ~0ull) return PKV_OK;
+  const int u = (int)(key >> 44), side = (int)((key >> 43) & 1), dim = (int)(key & 255);
+  const int64_t tok = (int64_t)((key >> 8) & ((1ull << 35) - 1));
+  if (where) { where[0] = u; where[1] = side; where[2] = tok; where[3] = dim; }
+  if (tok < c->prefill_tokens)  // engine.py:138
+    return fail(PKV_DATA, tok, "non-finite prefill %s element at token %lld, dim %d (unit %d)", side ? "V" : "K",
+                (long long)tok, dim, u);
+  return fail(PKV_DATA, tok, "non-finite decode vector at token %lld (unit %d)", (long long)tok, u);  // engine.py:181
 }
 
 static int reserve(pkv_cache* c, int64_t Tcap, int Pcap, cudaStream_t st) {
@@ -291,8 +319,12 @@ extern "C" int pkv_cache_create(const pkv_config* cfg, int32_t n_units, int32_t 
       dalloc(&d.probe, (size_t)n_units * 2 * 16 * 4) ||
       dalloc(&d.wk, (size_t)n_units * d.Wcap * head_dim * c->esize) ||
       dalloc(&d.wv, (size_t)n_units * d.Wcap * head_dim * c->esize) || dalloc(&c->scratch_flag, 8) ||
-      dalloc(&d.work, 16))
+      dalloc(&d.work, 16) || dalloc(&d.bad, 8))
     return bail(fail(PKV_CUDA, -1, "cudaMalloc failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if (cudaMemset(d.bad, 0xff, 8) != cudaSuccess || cudaHostAlloc((void**)&c->bad_host, 8, cudaHostAllocDefault) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->bad_ev, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(PKV_CUDA, -1, "non-finite flag allocation failed: %s", cudaGetErrorString(cudaGetLastError())));
+  *c->bad_host = ~0ull;
   if (flags & PKV_FLAG_STATS) {
     if (dalloc(&c->stats, 16)) return bail(fail(PKV_CUDA, -1, "cudaMalloc failed"));
     d.stats = c->stats;
@@ -320,6 +352,9 @@ extern "C" int pkv_cache_destroy(pkv_cache* c) {
                   d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag, d.work, c->mine_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (d.bad) cudaFree(d.bad);
+  if (c->bad_host) cudaFreeHost(c->bad_host);
+  if (c->bad_ev) cudaEventDestroy(c->bad_ev);
   delete c;
   return PKV_OK;
 }
@@ -372,6 +407,12 @@ extern "C" int pkv_cache_reset(pkv_cache* c, int32_t keep_patterns, void* stream
   c->nb_prefill = 0;
   c->decode_base = 0;
   c->blocks_stale = true;
+  c->prefill_tokens = 0;
+  CU(cudaMemsetAsync(c->dev.bad, 0xff, 8, st));
+  {
+    const int rc = publish_bad(c, st);
+    if (rc) return rc;
+  }
   if (!keep_patterns) {
     CU(cudaMemsetAsync(c->dev.nk, 0, (size_t)c->U * 4, st));
     CU(cudaMemsetAsync(c->dev.nv, 0, (size_t)c->U * 4, st));
@@ -684,6 +725,8 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
   const int64_t commit_n = T - std::min<int64_t>(T, W);
   int rc = reserve(c, std::max<int64_t>(c->dev.Tcap, T + 4 * G), c->dev.Pcap, st);
   if (rc) return rc;
+  CU(cudaMemsetAsync(c->dev.bad, 0xff, 8, st));  // a prefill starts a new stream of inputs
+  c->prefill_tokens = T;
   // mining (engine.py:156-159)
   int mask = 0;
   if (cfg.use_k_patterns && first_k) mask |= 1;
@@ -719,14 +762,15 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
     if (e1 != cudaSuccess) return e1;
     // window = newest min(T, W) rows (engine.py:166-167)
     const size_t off = (size_t)commit_n * c->D;
-    return launch_window_put<T_>(c->dev, (const T_*)k + off, (const T_*)v + off, T * c->D, (int)(T - commit_n), 0, st);
+    return launch_window_put<T_>(c->dev, (const T_*)k + off, (const T_*)v + off, T * c->D, (int)(T - commit_n), 0,
+                                 commit_n, st);
   });
   CU(e);
   c->win_slot0 = 0;
   c->win_len = (int)(T - commit_n);
   c->token_count = T;
   c->committed = commit_n;
-  return PKV_OK;
+  return publish_bad(c, st);
 }
 
 // ---------------------------------------------------------------------------------
@@ -738,6 +782,10 @@ extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stre
   const pkv_config& cfg = c->cfg;
   const int W = cfg.residual_window, G = cfg.group_size;
   DevCache& d = c->dev;
+  {  // a cache whose earlier input was non-finite refuses further appends (reset / prefill clears it)
+    int rc = check_bad(c, 0, nullptr);
+    if (rc) return rc;
+  }
   if (c->blocks_stale) {
     int rc = upload_blocks(c, st);
     if (rc) return rc;
@@ -746,7 +794,7 @@ extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stre
   const int slot = (c->win_slot0 + c->win_len) % d.Wcap;
   cudaError_t e = dispatch(c->dtype, [&](auto* tp) {
     using T_ = std::remove_pointer_t<decltype(tp)>;
-    return launch_window_put<T_>(d, (const T_*)k, (const T_*)v, c->D, 1, slot, st);
+    return launch_window_put<T_>(d, (const T_*)k, (const T_*)v, c->D, 1, slot, c->token_count, st);
   });
   CU(e);
   c->win_len += 1;
@@ -788,7 +836,12 @@ extern "C" int pkv_append(pkv_cache* c, const void* k, const void* v, void* stre
     c->win_slot0 = (c->win_slot0 + G) % d.Wcap;
     c->win_len -= G;
   }
-  return PKV_OK;
+  return publish_bad(c, st);
+}
+
+extern "C" int pkv_cache_check(pkv_cache* c, int32_t wait, int64_t* where) {
+  if (!c) return fail(PKV_USAGE, -1, "null cache");
+  return check_bad(c, wait, where);
 }
 
 // ---------------------------------------------------------------------------------
@@ -942,6 +995,7 @@ extern "C" int pkv_cache_fork_from(pkv_cache* dst, const pkv_cache* src, const i
   dst->nb_prefill = src->nb_prefill; dst->decode_base = src->decode_base;
   dst->blk_start = src->blk_start; dst->blk_len = src->blk_len;
   dst->pk_bound = src->pk_bound; dst->pv_bound = src->pv_bound;
+  dst->prefill_tokens = src->prefill_tokens;
   rc = upload_blocks(dst, st);
   if (rc) return rc;
   dst->blocks_stale = false;

@@ -40,6 +40,22 @@ template <> __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat1
 template <> __device__ __forceinline__ double to_f64<float>(float x) { return (double)x; }
 template <> __device__ __forceinline__ double to_f64<double>(double x) { return x; }
 
+// ---- non-finite inputs (engine.py:132-139, :180-181) ----------------------------------
+template <typename T> __device__ __forceinline__ bool is_finite_el(T x);
+template <> __device__ __forceinline__ bool is_finite_el<__half>(__half x) { return (__half_as_ushort(x) & 0x7c00u) != 0x7c00u; }
+template <> __device__ __forceinline__ bool is_finite_el<__nv_bfloat16>(__nv_bfloat16 x) {
+  return (__bfloat16_as_ushort(x) & 0x7f80u) != 0x7f80u;
+}
+template <> __device__ __forceinline__ bool is_finite_el<float>(float x) { return isfinite(x); }
+template <> __device__ __forceinline__ bool is_finite_el<double>(double x) { return isfinite(x); }
+// key of a non-finite input element: the smallest key is the reference's first DataError
+// location -- lowest unit, K before V (engine.py:151-152 checks K first), then token, then dim
+// (np.argwhere row-major order).  ~0 = none.
+__device__ __forceinline__ unsigned long long nf_key(int u, int side, int64_t token, int dim) {
+  return ((unsigned long long)u << 44) | ((unsigned long long)side << 43) | ((unsigned long long)token << 8) |
+         (unsigned long long)(dim & 255);
+}
+
 template <typename T> struct exact_in_f32 { static constexpr bool value = true; };
 template <> struct exact_in_f32<double> { static constexpr bool value = false; };
 
@@ -193,6 +209,7 @@ struct DevCache {
   // stats
   unsigned* stats;                // [0] fp64 refines, [1] exact-division fallbacks
   int* work;                      // [4] work-queue counters of the K1-TC encoder (reset per launch)
+  unsigned long long* bad;        // smallest nf_key of a non-finite input seen since the last prefill
 };
 
 // Source rows for an encode launch: row r of the span that starts `off` rows
@@ -247,7 +264,7 @@ struct ForkArenas {
 template <typename T> cudaError_t launch_encode(const DevCache&, const SpanSrc<T>&, const SpanSrc<T>&, int, int, cudaStream_t);
 template <typename T> cudaError_t launch_mine(const DevCache&, const MineArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_finite(const T*, int64_t, unsigned long long*, cudaStream_t);
-template <typename T> cudaError_t launch_window_put(const DevCache&, const T*, const T*, int64_t, int, int, cudaStream_t);
+template <typename T> cudaError_t launch_window_put(const DevCache&, const T*, const T*, int64_t, int, int, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_refresh(const DevCache&, int, int, int, cudaStream_t);
 template <typename T> cudaError_t launch_attn(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
 cudaError_t launch_dequant(const DevCache&, int, int64_t, int64_t, double*, double*, cudaStream_t);

@@ -586,6 +586,9 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
   const int64_t off = start - c.blk_start[first_block];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int D = c.D, Dp = c.Dp;
+  // prefill spans read caller rows (finiteness checked here); decode flushes read window rows
+  // that window_put already checked
+  const bool check_nf = srck.ring > (int64_t)1 << 40;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EncSmem sm;
@@ -662,11 +665,14 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
             if (r < L) {
               const T* e = reinterpret_cast<const T*>(&v[k]);
               float fv[EPV];
+              unsigned nf = 0u;
 #pragma unroll
               for (int q2 = 0; q2 < EPV; ++q2) {
                 fv[q2] = (float)to_f64(e[q2]);
                 m = fmaxf(m, fabsf(fv[q2]));
+                if (check_nf && !is_finite_el(e[q2])) nf |= 1u << q2;
               }
+              if (nf) atomicMin(c.bad, nf_key(u, side, start + r, vl * EPV + __ffs(nf) - 1));
               float* xr = sm.xs + r * sm.DS + vl * EPV;
               if constexpr (EPV % 4 == 0) {
 #pragma unroll
@@ -690,6 +696,7 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
             const float f = (float)to_f64(row[ch]);
             xr[ch] = f;
             m = fmaxf(m, fabsf(f));
+            if (check_nf && !is_finite_el(row[ch])) atomicMin(c.bad, nf_key(u, side, start + r, ch));
           }
           m = warp_max_f(m);
           if (lane == 0) sm.xabs[r] = m;

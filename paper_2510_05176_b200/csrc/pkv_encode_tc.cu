@@ -545,10 +545,25 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
 // bounds, survivors, fp64 re-match.  Leaves the final pattern index in sc.fidx() and the
 // keyed statistics of the final residual in sc.kmx()/kmn/xmx/xmn(/info).
 // ---------------------------------------------------------------------------------------
+// A non-finite score row means a non-finite x element: every pattern column accumulates
+// x_c * m'_c over all channels and Inf * 0 = NaN, while finite fp16 x and m' cannot overflow
+// fp32 (|x.m'| <= 128 * 65504^2).  Rare path: scan the token's row for the first bad channel.
+__device__ __noinline__ void nonfinite_row(const unsigned char* X, int t, bool flagged, int side, int u,
+                                           int64_t start, unsigned long long* bad) {
+  SMEM_PTR(X);
+  if (!flagged) return;
+  for (int ch = 0; ch < 128; ++ch)
+    if (!isfinite(xt_at(X, t, ch))) {
+      atomicMin(bad, nf_key(u, side, start + t, ch));
+      return;
+    }
+}
+
 template <int SIDE>
 __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X, const float* M,
                                          uint64_t* mmab, uint32_t ph, uint32_t tcol, int w, int lane, int P, float pmx,
-                                         const double* p64, unsigned* stats) {
+                                         const double* p64, unsigned* stats, int u, int64_t start, int L,
+                                         unsigned long long* bad) {
   SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base);
   warp_converged();
   const int g = lane >> 2, q = lane & 3;
@@ -564,6 +579,10 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
     tmem_ld8(tl + p0, v);
     tmem_ld8(tl + p0 + 8, v2);
     tmem_ld_wait();
+    if (p0 == 0) {  // fused finiteness check of the token's x row (engine.py:136-138)
+      const bool nf = !(fabsf(__uint_as_float(v[0])) <= 3.0e38f);
+      if (__any_sync(0xffffffffu, nf)) nonfinite_row(X, tt_, nf && tt_ < L, SIDE, u, start, bad);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       best = fminf(best, fkey(__fmaf_rn(-2.f, __uint_as_float(v[i]), pt.bb()[p0 + i]), p0 + i, 0xffffffe0u));
@@ -1173,7 +1192,7 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         }
         mma_commit(mmab);
       }
-      token_stage<SIDE>(sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats);
+      token_stage<SIDE>(sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats, u, start, L, c.bad);
       const __half* xsrc = A.src[SIDE] + (int64_t)u * A.unit_stride + (start - row0) * 128;
       const int64_t blk = (int64_t)u * c.NBcap + b;
       const int64_t nxt = it + 4 < i1 ? it + 4 : (j0 + sg < j1 ? j0 + sg : -1);

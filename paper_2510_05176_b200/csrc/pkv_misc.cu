@@ -32,29 +32,36 @@ template cudaError_t launch_finite<float>(const float*, int64_t, unsigned long l
 template cudaError_t launch_finite<double>(const double*, int64_t, unsigned long long*, cudaStream_t);
 
 // ---- window ring: copy rows [U][nrows][D] into ring slots (slot0 + r) % Wcap -------
+// Row r is token token0 + r of its unit; non-finite elements are flagged in c.bad (the
+// reference's finiteness checks, engine.py:136-138 / 180-181, fused into the copy).
 template <typename T>
-__global__ void window_put_kernel(DevCache c, const T* k, const T* v, int64_t src_unit_stride, int nrows, int slot0) {
+__global__ void window_put_kernel(DevCache c, const T* k, const T* v, int64_t src_unit_stride, int nrows, int slot0,
+                                  int64_t token0) {
   const int u = blockIdx.y;
   const int64_t n = (int64_t)nrows * c.D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / c.D), ch = (int)(i - (int64_t)r * c.D);
     const int64_t dst = ((int64_t)u * c.Wcap + (slot0 + r) % c.Wcap) * c.D + ch;
     const int64_t src = (int64_t)u * src_unit_stride + i;
-    reinterpret_cast<T*>(c.wk)[dst] = k[src];
-    reinterpret_cast<T*>(c.wv)[dst] = v[src];
+    const T kv = k[src], vv = v[src];
+    reinterpret_cast<T*>(c.wk)[dst] = kv;
+    reinterpret_cast<T*>(c.wv)[dst] = vv;
+    if (!is_finite_el(kv)) atomicMin(c.bad, nf_key(u, 0, token0 + r, ch));
+    if (!is_finite_el(vv)) atomicMin(c.bad, nf_key(u, 1, token0 + r, ch));
   }
 }
 template <typename T>
-cudaError_t launch_window_put(const DevCache& c, const T* k, const T* v, int64_t sus, int nrows, int slot0, cudaStream_t st) {
+cudaError_t launch_window_put(const DevCache& c, const T* k, const T* v, int64_t sus, int nrows, int slot0, int64_t token0,
+                              cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
   int gx = (int)imin64(((int64_t)nrows * c.D + 255) / 256, 64);
-  window_put_kernel<T><<<dim3(gx, c.U), 256, 0, st>>>(c, k, v, sus, nrows, slot0);
+  window_put_kernel<T><<<dim3(gx, c.U), 256, 0, st>>>(c, k, v, sus, nrows, slot0, token0);
   return cudaGetLastError();
 }
-template cudaError_t launch_window_put<__half>(const DevCache&, const __half*, const __half*, int64_t, int, int, cudaStream_t);
-template cudaError_t launch_window_put<__nv_bfloat16>(const DevCache&, const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int, int, cudaStream_t);
-template cudaError_t launch_window_put<float>(const DevCache&, const float*, const float*, int64_t, int, int, cudaStream_t);
-template cudaError_t launch_window_put<double>(const DevCache&, const double*, const double*, int64_t, int, int, cudaStream_t);
+template cudaError_t launch_window_put<__half>(const DevCache&, const __half*, const __half*, int64_t, int, int, int64_t, cudaStream_t);
+template cudaError_t launch_window_put<__nv_bfloat16>(const DevCache&, const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int, int, int64_t, cudaStream_t);
+template cudaError_t launch_window_put<float>(const DevCache&, const float*, const float*, int64_t, int, int, int64_t, cudaStream_t);
+template cudaError_t launch_window_put<double>(const DevCache&, const double*, const double*, int64_t, int, int, int64_t, cudaStream_t);
 
 // ---- flush refresh: midrange of the oldest G ring rows appended as a pattern -------
 // grid (U, 2 sides), block D threads.  0.5 * (min + max) in IEEE fp64.

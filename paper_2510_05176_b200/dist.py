@@ -55,7 +55,7 @@ def gather_head_outputs(local: torch.Tensor, group=None) -> torch.Tensor:
 
     local: [B, L, Hkv_local, G, d] on this rank -> [B, L, Hkv, G, d] with rank r's
     heads at [r*Hkv_local, (r+1)*Hkv_local)."""
-    world = dist.get_world_size(group)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return local
     dev = local.device
@@ -89,7 +89,7 @@ def lse_merge(o: torch.Tensor, m: torch.Tensor, l: torch.Tensor) -> torch.Tensor
 def gather_and_merge_partials(o: torch.Tensor, m: torch.Tensor, l: torch.Tensor, group=None) -> torch.Tensor:
     """Sequence-split decode attention: every rank holds a token range of the
     same heads; exchange (o, m, l) once and LSE-merge locally."""
-    world = dist.get_world_size(group)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return lse_merge(o[None], m[None], l[None])
     packed = torch.cat([o.reshape(-1), m.reshape(-1), l.reshape(-1)])

@@ -249,3 +249,51 @@ def test_reset_then_decode_only(pkv):
         heads.append(h)
     assert cache.info().n_blocks == 1 and cache.block_table()[0].tolist() == [0]
     _assert_matches_oracle(cache, heads)
+
+
+@pytest.mark.parametrize("dtype", ["float16", "float32"])
+def test_fused_nonfinite_detection(pkv, dtype):
+    """engine.py:136-138 / 180-181 fused into the kernels: K1-TC's tensor-core scores (fp16) /
+    K1's staging (fp32) and the window copy flag the first non-finite element -- lowest unit,
+    K before V, then token, dim -- and it surfaces as DataError with the reference's message,
+    deferred (check(), the next append) or at once (sync_check); reset clears it."""
+    from paper_2510_05176_b200.config import EngineConfig
+    from paper_2510_05176_b200.errors import DataError
+
+    tdt = getattr(torch, dtype)
+    U, T, d = 3, 1000, 128
+    k, v = _units(U, T + 4, d, seed=31)
+    cfg = EngineConfig(bits=2, pattern_count=16)
+    cache = pkv.PatternKVCache(cfg, U, d, dtype=tdt, max_tokens=2048)
+    kt = torch.from_numpy(k).to("cuda", tdt)
+    vt = torch.from_numpy(v).to("cuda", tdt)
+    # committed-span elements (encoder) and a window element
+    kt2, vt2 = kt.clone(), vt.clone()
+    vt2[1, 500, 7] = float("nan")
+    kt2[2, 100, 3] = float("inf")
+    kt2[1, T - 5, 9] = -float("inf")  # window row of unit 1: K before V wins within the unit
+    cache.prefill(kt2[:, :T], vt2[:, :T])
+    torch.cuda.synchronize()
+    with pytest.raises(DataError, match=r"non-finite prefill K element at token 995, dim 9 \(unit 1\)"):
+        cache.check()
+    with pytest.raises(DataError):
+        cache.append(kt[:, T], vt[:, T])  # a flagged cache refuses appends
+    # committed-span only
+    cache.reset(keep_patterns=False)
+    vt3 = vt.clone()
+    vt3[0, 300, 127] = float("nan")
+    with pytest.raises(DataError, match=r"non-finite prefill V element at token 300, dim 127 \(unit 0\)"):
+        cache.prefill(kt[:, :T], vt3[:, :T], sync_check=True)
+    # clean prefill, then a non-finite decode vector
+    cache.reset(keep_patterns=False)
+    cache.prefill(kt[:, :T], vt[:, :T], sync_check=True)
+    bad_k = kt[:, T].clone()
+    bad_k[2, 5] = float("nan")
+    cache.append(bad_k, vt[:, T])
+    with pytest.raises(DataError, match=rf"non-finite decode vector at token {T} \(unit 2\)"):
+        cache.check()
+    # the clean path stays clean
+    cache.reset(keep_patterns=False)
+    cache.prefill(kt[:, :T], vt[:, :T], sync_check=True)
+    for t in range(T, T + 4):
+        cache.append(kt[:, t], vt[:, t], sync_check=True)

@@ -210,7 +210,7 @@ def test_errors_map_to_reference_taxonomy(pkv):
     v = torch.zeros((1, 10, 4), dtype=torch.float64)
     v[0, 3, 1] = float("inf")
     with pytest.raises(DataError, match="token 3"):
-        cache.prefill(k, v, validate=True)
+        cache.prefill(k, v, sync_check=True)
 
 
 @pytest.mark.parametrize("k", [16, 32, 64])
