@@ -152,7 +152,7 @@ struct pkv_cache {
 // labels out (i32), history [U][2][25] f64, niter [U][2] i32, first [U][2] i64
 static size_t mine_scratch_need(int U, int64_t T) {
   const size_t n2 = (size_t)U * 2 * T;
-  return n2 * 8 * 2 + n2 * 4 * 4 + (size_t)U * 2 * 25 * 8 + (size_t)U * 2 * 4 + (size_t)U * 2 * 8 + 8 * 64;
+  return n2 * 8 * 2 + n2 * 4 * 4 + (size_t)U * 2 * 25 * 8 + (size_t)U * 2 * 4 + (size_t)U * 2 * 8 + 9 * 256;  // + carve alignment
 }
 
 static int esize_of(int dtype) {
