@@ -640,6 +640,657 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
   }
 }
 
+// =================================================================================
+// K2 v2: streamed k-means (fp16 points, d = 128, k <= 48), one CTA per unit-side.
+// Every pass over the points is one TMA stream of 128-point tiles through a 3-stage
+// smem ring, consumed by 4 row warps (thread per point) and 4 channel warps (thread
+// per channel), so a Lloyd round costs ONE pass instead of three:
+//   * labels of round r on tcgen05 (distance GEMM vs the centers split hi + lo, TMEM
+//     accumulator, fp64 re-decision of near ties) -- as in the v1 kernel;
+//   * the objective of round r-1, sum_t ||x_t - c_r[l_{r-1}(t)]||^2 (patterns.py:121:
+//     the new means against the previous labels), fp64 from the smem tile;
+//   * the centroid sums of round r by the channel warps from the same tile.
+// The sums are exact in fp64 whenever T * max|x| < 2^29: fp16 values are multiples of
+// 2^-24, so every partial sum of at most T of them is a multiple of 2^-24 below 2^53 *
+// 2^-24 and every fp64 addition is exact -- the result is independent of the order and
+// equals numpy's sequential axis-0 sum bit for bit (accumulators start at -0.0, so an
+// all -0.0 column keeps its sign as numpy's first-row start does).  Otherwise (and after
+// an empty-cluster repair) the sums are recomputed in numpy's point order (v1 code).
+// Farthest-point seeding streams the same ring: fp64 distances to the newest seed from
+// the smem tile, running minima in HBM, block argmax (lowest index on ties).
+// A round's objective is known one pass late, so the stop rule (patterns.py:123) of
+// round r-1 is applied after pass r: the labels/sums pass r also produced are dropped.
+// =================================================================================
+constexpr int SK_THREADS = 384;   // warp 0 TMA, 1 MMA, 2-3 idle, 4-7 rows, 8-11 channels
+constexpr int SK_NS = 3;          // smem ring stages
+constexpr int SK_ROW0 = 4, SK_CH0 = 8;
+constexpr int SK_KMAX = 48;
+
+struct SkSmem {
+  unsigned char* sA;   // [NS][2 halves][128 rows x 128 B] swizzled fp16 tiles
+  unsigned char* sB;   // [2 halves][NP rows x 128 B]
+  double* cen;         // [k][129]
+  double* acc;         // [k][128] centroid sums
+  double* seed;        // [128] newest seed row (fp64)
+  int* labs;           // [NS][128] labels of the tile's rows (row -> channel warps)
+  float* cc;           // [NP/2]
+  int* cnt;            // [k]
+  int* off;            // [k]
+  int* flags;          // [8]
+  double* redv;        // [16]
+  long long* redi;     // [16]
+  uint64_t* bars;      // full[NS], empty[NS], lready[NS], tfull[2], tempty[2]
+  uint32_t* tmem;
+};
+__host__ __device__ inline size_t sk_smem_bytes(int k) {
+  const int NP = ((2 * k + 15) / 16) * 16;
+  return 1024 + (size_t)SK_NS * 2 * 16384 + 2 * (size_t)NP * 128 + (size_t)k * 129 * 8 + (size_t)k * 128 * 8 + 128 * 8 +
+         SK_NS * 128 * 4 + (size_t)NP / 2 * 4 + 2 * (size_t)k * 4 + 8 * 4 + 16 * 8 + 16 * 8 + (3 * SK_NS + 4) * 8 + 16 + 64 +
+         14 * 16;  // 16-byte carve alignment
+}
+__device__ __forceinline__ unsigned char* sk_tile(const SkSmem& s, int stage, int half) {
+  return s.sA + (stage * 2 + half) * 16384;
+}
+#define SK_SMEM(p) __builtin_assume(__isShared(p))
+__device__ __forceinline__ double h2d(__half h) {  // one F2F.F64.F16
+  double r;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(__half_as_ushort(h)));
+  return r;
+}
+// fp64 squared distance of tile row `row` to a fp64 row `cj`, channel order, one fma
+// chain (the v1 arithmetic; used for the near-tie label decisions)
+__device__ __forceinline__ double sk_d2(const unsigned char* tile, int row, const double* cj) {
+  SK_SMEM(tile); SK_SMEM(cj);
+  double a0 = 0.0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const unsigned char* base = tile + half * 16384 + row * 128;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + ((ch ^ (row & 7)) << 4));
+      const __half* h = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double d = __dsub_rn(h2d(h[e]), cj[half * 64 + ch * 8 + e]);
+        a0 = fma(d, d, a0);
+      }
+    }
+  }
+  return a0;
+}
+// the same distance with four independent accumulators (a 32-deep instead of a 128-deep
+// dependency chain: seeding minima and the objective); |x|max of the row on request
+template <bool XMAX>
+__device__ __forceinline__ double sk_d2x4(const unsigned char* tile, int row, const double* cj, float* xmax) {
+  SK_SMEM(tile); SK_SMEM(cj);
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  float xm = 0.f;
+#pragma unroll 4
+  for (int q = 0; q < 16; ++q) {  // 16-byte chunk q = channels 8q .. 8q+7
+    const int half = q >> 3, ch = q & 7;
+    const uint4 v = *reinterpret_cast<const uint4*>(tile + half * 16384 + row * 128 + ((ch ^ (row & 7)) << 4));
+    const __half* h = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (XMAX) xm = fmaxf(xm, fabsf(__half2float(h[e])));
+      const double d = __dsub_rn(h2d(h[e]), cj[8 * q + e]);
+      a[e & 3] = fma(d, d, a[e & 3]);
+    }
+  }
+  if (XMAX) *xmax = fmaxf(*xmax, xm);
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+struct SkCounters { uint32_t gt, gm, gl; };  // tiles streamed, MMA tiles, label hand-offs
+
+enum { SK_SEED = 1, SK_ASSIGN = 2, SK_OBJ = 4, SK_SUMS = 8, SK_FIRST = 16 };
+
+// Block reductions over the 8 consumer warps (rows 4-7 carry the values; others pass identity)
+__device__ __forceinline__ double sk_block_sum(double v, const SkSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sm.redv[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < SK_THREADS / 32; ++w) r += sm.redv[w];
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ void sk_block_argmax(double v, long long i, const SkSmem& sm, double& ov, long long& oi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_argmax_d(v, i);
+  if (lane == 0) { sm.redv[warp] = v; sm.redi[warp] = i; }
+  __syncthreads();
+  ov = -1.0 / 0.0;
+  oi = 0x7fffffffffffffffLL;
+  for (int w = 0; w < SK_THREADS / 32; ++w) {
+    const double v2 = sm.redv[w];
+    const long long i2 = sm.redi[w];
+    if (v2 > ov || (v2 == ov && i2 < oi)) { ov = v2; oi = i2; }
+  }
+  __syncthreads();
+}
+
+// One streamed pass.  Returns, on row threads, this thread's share of the objective
+// (SK_OBJ) and its running argmax of the seeding minima (SK_SEED via bv/bi) and |x|max.
+__device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUtensorMap* map, int64_t row_base,
+                        SkCounters& ctr, double* near_, const int* lab_old, int* lab_new, double& obj, double& bv,
+                        long long& bi_out, float& xmax) {
+  using namespace sm100;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (int)((Tn + 127) / 128);
+  const int NP = ((2 * k + 15) / 16) * 16;
+  uint64_t* full = sm.bars;
+  uint64_t* empty = sm.bars + SK_NS;
+  uint64_t* lready = sm.bars + 2 * SK_NS;
+  uint64_t* tfull = sm.bars + 3 * SK_NS;
+  uint64_t* tempty = sm.bars + 3 * SK_NS + 2;
+  const bool assign = mode & SK_ASSIGN, sums = mode & SK_SUMS;
+  if (assign) {
+    for (int j = tid; j < k; j += SK_THREADS) sm.cnt[j] = 0;
+    // B operand: row 2j = hi(c_j), row 2j+1 = lo(c_j) = fp16(c_j - hi), K-major, 128B swizzle
+    for (int i = tid; i < NP * 16; i += SK_THREADS) {
+      const int row = i >> 4, half = (i >> 3) & 1, chunk = i & 7;
+      const int j = row >> 1, part = row & 1;
+      __half hv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        __half h = __float2half(0.f);
+        if (j < k) {
+          const double cv = sm.cen[j * 129 + half * 64 + chunk * 8 + e];
+          const __half hi = __double2half(cv);
+          h = part == 0 ? hi : __double2half(cv - (double)__half2float(hi));
+        }
+        hv[e] = h;
+      }
+      *reinterpret_cast<uint4*>(sm.sB + half * NP * 128 + row * 128 + ((chunk ^ (row & 7)) << 4)) =
+          *reinterpret_cast<const uint4*>(hv);
+    }
+    for (int j = tid; j < NP / 2; j += SK_THREADS) {
+      double a = 0.0;
+      if (j < k)
+        for (int c = 0; c < 128; ++c) a = fma(sm.cen[j * 129 + c], sm.cen[j * 129 + c], a);
+      sm.cc[j] = j < k ? (float)a : __int_as_float(0x7f800000);
+    }
+  }
+  if (sums)
+    for (int i = tid; i < k * 128; i += SK_THREADS) sm.acc[i] = -0.0;
+  fence_proxy_async();
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int m = 0; m < NT; ++m) {
+        const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], 2 * 16384);
+        const int r0 = (int)(row_base + (int64_t)m * 128);
+        tma_load_2d(sk_tile(sm, s, 0), map, &full[s], 0, r0);
+        tma_load_2d(sk_tile(sm, s, 1), map, &full[s], 64, r0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (assign && lane == 0) {
+      const uint32_t idesc = idesc_f16_f32(128, NP);
+      const uint64_t db0 = smem_desc_k_sw128(sm.sB), db1 = smem_desc_k_sw128(sm.sB + NP * 128);
+      for (int m = 0; m < NT; ++m) {
+        const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
+        const uint32_t gm = ctr.gm + m, acc = gm & 1, aph = (gm >> 1) & 1;
+        mbar_wait(&full[s], ph);
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint64_t da0 = smem_desc_k_sw128(sk_tile(sm, s, 0)), da1 = smem_desc_k_sw128(sk_tile(sm, s, 1));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t da = (kk < 4 ? da0 : da1) + 2 * (kk & 3);
+          const uint64_t db = (kk < 4 ? db0 : db1) + 2 * (kk & 3);
+          mma_f16_ss(*sm.tmem + acc * 128, da, db, idesc, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= SK_ROW0 && warp < SK_ROW0 + 4) {
+    const int q = warp & 3, row = 32 * q + lane;
+    float ccmax = 0.f;
+    if (assign)
+      for (int j = 0; j < k; ++j) ccmax = fmaxf(ccmax, sm.cc[j]);
+    const float cnorm = sqrtf(ccmax);
+    for (int m = 0; m < NT; ++m) {
+      const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
+      const int64_t t = (int64_t)m * 128 + row;
+      const bool live = t < Tn;
+      const unsigned char* tile = sk_tile(sm, s, 0);
+      int bi = 0;
+      float vb = __int_as_float(0x7f800000), vs = vb;
+      mbar_wait(&full[s], ph);
+      if (assign) {
+        const uint32_t gm = ctr.gm + m, acc = gm & 1, aph = (gm >> 1) & 1;
+        const uint32_t tbase = *sm.tmem + acc * 128 + ((uint32_t)(32 * q) << 16);
+        // |x|^2 for the error bound (the tile has landed: the MMA consumed it)
+        float xq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const unsigned char* base = tile + half * 16384 + row * 128;
+          SK_SMEM(base);
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const uint4 w = *reinterpret_cast<const uint4*>(base + ((ch ^ (row & 7)) << 4));
+            const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(h2[e]);
+              xq[e] = fmaf(f.x, f.x, fmaf(f.y, f.y, xq[e]));
+            }
+          }
+        }
+        const float xx = (xq[0] + xq[1]) + (xq[2] + xq[3]);
+        // same error bound as the v1 tensor-core pass (K2)
+        const float tol = 1.52587890625e-05f * sqrtf(xx) * cnorm + 4.76837158203125e-07f * (ccmax + xx);
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < NP; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tbase + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int j = c0 / 2 + e;
+            if (j < k) {
+              const float dot = __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]);
+              const float val = fmaf(-2.f, dot, sm.cc[j]);
+              if (val < vb) { vs = vb; vb = val; bi = j; }
+              else vs = fminf(vs, val);
+            }
+          }
+        }
+        // near tie: fp64 over the candidates inside the error window only (every other center
+        // is provably farther), lowest index among equal fp64 distances
+        const bool tie = live && vs - vb <= 2.f * tol;
+        if (__any_sync(0xffffffffu, tie)) {
+          const float lim = vb + 2.f * tol;
+          double best = __longlong_as_double(0x7ff0000000000000LL);
+          int bj = bi;
+#pragma unroll 1
+          for (int c0 = 0; c0 < NP; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tbase + c0, v);  // warp-collective reload
+            tmem_ld_wait();
+            uint32_t cand = 0u;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int j = c0 / 2 + e;
+              if (j < k && fmaf(-2.f, __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]), sm.cc[j]) <= lim)
+                cand |= 1u << e;
+            }
+            if (!tie) cand = 0u;
+            while (cand) {
+              const int j = c0 / 2 + __ffs(cand) - 1;
+              cand &= cand - 1;
+              const double d = sk_d2x4<false>(tile, row, sm.cen + j * 129, nullptr);
+              if (d < best) { best = d; bj = j; }
+            }
+          }
+          bi = bj;
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
+      if (live) {
+        if (mode & SK_SEED) {
+          const double d = (mode & SK_FIRST) ? sk_d2x4<true>(tile, row, sm.seed, &xmax)
+                                             : sk_d2x4<false>(tile, row, sm.seed, nullptr);
+          const double nv = (mode & SK_FIRST) ? d : fmin(near_[t], d);
+          near_[t] = nv;
+          if (nv > bv) { bv = nv; bi_out = t; }
+        }
+        if (assign) {
+          lab_new[t] = bi;
+          atomicAdd(&sm.cnt[bi], 1);
+        }
+        if (mode & SK_OBJ) obj += sk_d2x4<false>(tile, row, sm.cen + lab_old[t] * 129, nullptr);
+      }
+      if (sums) {  // label hand-off slot/barrier follow their own counter (gl), not the tile stage
+        const uint32_t ls = (ctr.gl + m) % SK_NS;
+        sm.labs[ls * 128 + row] = live ? bi : -1;
+        mbar_arrive(&lready[ls]);
+      }
+      mbar_arrive(&empty[s]);
+    }
+  } else if (warp >= SK_CH0 && warp < SK_CH0 + 4) {
+    const int c = tid - 32 * SK_CH0;  // channel
+    const int hoff = (c >> 6) * 16384 + ((c & 7) << 1), cb = (c & 63) >> 3;
+    for (int m = 0; m < NT; ++m) {
+      const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
+      if (sums) {
+        const uint32_t gl = ctr.gl + m, ls = gl % SK_NS, lph = (gl / SK_NS) & 1;
+        mbar_wait(&lready[ls], lph);
+        const unsigned char* tile = sk_tile(sm, s, 0) + hoff;
+        const int* lb = sm.labs + ls * 128;
+        double* accc = sm.acc + c;
+        SK_SMEM(tile); SK_SMEM(lb); SK_SMEM(accc);
+        // rows in blocks of 8: labels and values load up front; the current label's run is
+        // summed in two interleaved registers (exact sums: any order) and flushed on a change
+        int curj = -1;
+        double run0 = -0.0, run1 = -0.0;
+        for (int r0 = 0; r0 < 128; r0 += 8) {
+          const int4 la = *reinterpret_cast<const int4*>(lb + r0);
+          const int4 lb4 = *reinterpret_cast<const int4*>(lb + r0 + 4);
+          const int js[8] = {la.x, la.y, la.z, la.w, lb4.x, lb4.y, lb4.z, lb4.w};
+          double xs[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int r = r0 + e;
+            xs[e] = h2d(*reinterpret_cast<const __half*>(tile + r * 128 + ((cb ^ (r & 7)) << 4)));
+          }
+          bool same = curj >= 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) same &= js[e] == curj;
+          if (same) {  // the whole block continues the current run (uniform over the warp)
+            run0 = __dadd_rn(run0, __dadd_rn(__dadd_rn(xs[0], xs[1]), __dadd_rn(xs[2], xs[3])));
+            run1 = __dadd_rn(run1, __dadd_rn(__dadd_rn(xs[4], xs[5]), __dadd_rn(xs[6], xs[7])));
+            continue;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int j = js[e];
+            if (j < 0) continue;  // past Tn
+            if (j != curj) {
+              if (curj >= 0) accc[curj * 128] = __dadd_rn(accc[curj * 128], __dadd_rn(run0, run1));
+              curj = j;
+              run0 = xs[e];
+              run1 = -0.0;
+            } else if (e & 1) {
+              run1 = __dadd_rn(run1, xs[e]);
+            } else {
+              run0 = __dadd_rn(run0, xs[e]);
+            }
+          }
+        }
+        if (curj >= 0) accc[curj * 128] = __dadd_rn(accc[curj * 128], __dadd_rn(run0, run1));
+      } else {
+        mbar_wait(&full[s], ph);
+      }
+      mbar_arrive(&empty[s]);
+    }
+  }
+  ctr.gt += NT;
+  if (assign) ctr.gm += NT;
+  if (sums) ctr.gl += NT;
+  __syncthreads();
+}
+
+// centroid sums in numpy's point order straight from HBM (v1 order; any data)
+__device__ void sk_seq_sums(const __half* X, int64_t Tn, int k, const int* lab, const SkSmem& sm) {
+  const int tid = threadIdx.x;
+  if (tid < 128) {
+    const int c = tid;
+    for (int j = 0; j < k; ++j) sm.acc[j * 128 + c] = 0.0;
+    uint64_t started = 0ull;  // k <= 48
+    int curj = -1;
+    double racc = 0.0;
+    for (int64_t t = 0; t < Tn; ++t) {
+      const int jt = lab[t];
+      const double x = (double)__half2float(X[t * 128 + c]);
+      if (jt == curj) {
+        racc = __dadd_rn(racc, x);
+      } else {
+        if (curj >= 0) sm.acc[curj * 128 + c] = racc;
+        racc = ((started >> jt) & 1ull) ? __dadd_rn(sm.acc[jt * 128 + c], x) : x;
+        started |= 1ull << jt;
+        curj = jt;
+      }
+    }
+    if (curj >= 0) sm.acc[curj * 128 + c] = racc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SK_THREADS, 1)
+kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, int side0, int nsides) {
+  using namespace sm100;
+  // K sides first (they run ~25 rounds, V ~2): longest-first over the waves
+  const int side = side0 + (int)blockIdx.x / c.U, u = (int)blockIdx.x % c.U;
+  (void)nsides;
+  const int k = a.k, tid = threadIdx.x, warp = tid >> 5;
+  const int64_t Tn = a.T;
+  const __half* X = a.x[side] + (int64_t)u * a.unit_stride;
+  const int64_t so = ((int64_t)u * 2 + side) * Tn;
+  double* near_ = a.near_ + so;
+  double* own = a.own + so;
+  int* lab = a.lab + so;
+  int* lab2 = a.lab2 + so;
+  double* hist = a.hist + ((int64_t)u * 2 + side) * 25;
+  double* p64 = (side == 0 ? c.kpat64 : c.vpat64) + (int64_t)u * c.Pcap * 128;
+  float* p32 = (side == 0 ? c.kpat32 : c.vpat32) + (int64_t)u * c.Pcap * c.Dp;
+  const CUtensorMap* map = side == 0 ? &tmK : &tmV;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SkSmem sm;
+  {
+    const int NP = ((2 * k + 15) / 16) * 16;
+    // 1024-aligned base as pointer arithmetic on the shared array (keeps the address space
+    // visible to the compiler: plain LDS/STS, and the SK_SMEM assumptions hold)
+    unsigned char* p = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    auto carve = [&](size_t bytes) { unsigned char* q = p; p += (bytes + 15) & ~(size_t)15; return q; };
+    sm.sA = carve(SK_NS * 2 * 16384);
+    sm.sB = carve(2 * NP * 128);
+    sm.cen = reinterpret_cast<double*>(carve((size_t)k * 129 * 8));
+    sm.acc = reinterpret_cast<double*>(carve((size_t)k * 128 * 8));
+    sm.seed = reinterpret_cast<double*>(carve(128 * 8));
+    sm.redv = reinterpret_cast<double*>(carve(16 * 8));
+    sm.redi = reinterpret_cast<long long*>(carve(16 * 8));
+    sm.bars = reinterpret_cast<uint64_t*>(carve((3 * SK_NS + 4) * 8));
+    sm.labs = reinterpret_cast<int*>(carve(SK_NS * 128 * 4));
+    sm.cc = reinterpret_cast<float*>(carve(NP / 2 * 4));
+    sm.cnt = reinterpret_cast<int*>(carve(k * 4));
+    sm.off = reinterpret_cast<int*>(carve(k * 4));
+    sm.flags = reinterpret_cast<int*>(carve(8 * 4));
+    sm.tmem = reinterpret_cast<uint32_t*>(p);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < SK_NS; ++i) {
+      mbar_init(&sm.bars[i], 1);                 // full: producer arrive + tx
+      mbar_init(&sm.bars[SK_NS + i], 256);       // empty: row + channel threads
+      mbar_init(&sm.bars[2 * SK_NS + i], 128);   // lready: row threads
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.bars[3 * SK_NS + i], 1);     // tmem full: MMA commit
+      mbar_init(&sm.bars[3 * SK_NS + 2 + i], 128);  // tmem empty: row threads
+    }
+    fence_mbar_init();
+    tma_prefetch(map);
+  }
+  if (warp == 1) tmem_alloc<256>(sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  SkCounters ctr{0u, 0u, 0u};
+  const int64_t row_base = (int64_t)u * Tn;
+  double objp = 0.0, bv = -1.0 / 0.0;
+  long long bi = 0x7fffffffffffffffLL;
+  float xmax = 0.f;
+
+  // ---- seeding (patterns.py:134-142) with distinct-rows detection -------------------
+  const int64_t first = a.first[side][u];
+  int* chosen = sm.off;  // seed indices (k)
+  if (tid == 0) chosen[0] = (int)first;
+  for (int c2 = tid; c2 < 128; c2 += SK_THREADS) sm.seed[c2] = (double)__half2float(X[first * 128 + c2]);
+  __syncthreads();
+  sk_pass(SK_SEED | SK_FIRST, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
+  double vmax;
+  long long imax;
+  sk_block_argmax(bv, bi, sm, vmax, imax);
+  // exact-sum condition: T * max|x| < 2^29 (see the header)
+  {
+    float xm = warp_max_f(xmax);
+    if ((tid & 31) == 0) sm.redv[warp] = xm;
+    __syncthreads();
+    float m = 0.f;
+    for (int w = 0; w < SK_THREADS / 32; ++w) m = fmaxf(m, (float)sm.redv[w]);
+    __syncthreads();
+    xmax = m;
+  }
+  const bool exact_sums = (double)xmax * (double)Tn < 536870912.0;
+  int n = 1;
+  bool shortcut = false;
+  while (true) {
+    if (vmax == 0.0) { shortcut = true; break; }
+    if (n == k) break;
+    if (tid == 0) chosen[n] = (int)imax;
+    ++n;
+    for (int c2 = tid; c2 < 128; c2 += SK_THREADS) sm.seed[c2] = (double)__half2float(X[imax * 128 + c2]);
+    __syncthreads();
+    bv = -1.0 / 0.0;
+    bi = 0x7fffffffffffffffLL;
+    sk_pass(SK_SEED, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
+    sk_block_argmax(bv, bi, sm, vmax, imax);
+  }
+
+  int iters = 0;
+  int* fin = lab;
+  if (shortcut) {
+    // np.unique(axis=0): the n distinct rows in lexicographic order, labels = nearest
+    for (int i = tid; i < n; i += SK_THREADS) {
+      const __half* ri = X + (int64_t)chosen[i] * 128;
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        if (j == i) continue;
+        const __half* rj = X + (int64_t)chosen[j] * 128;
+        for (int cc = 0; cc < 128; ++cc) {
+          const float x1 = __half2float(rj[cc]), x2 = __half2float(ri[cc]);
+          if (x1 < x2) { ++rank; break; }
+          if (x1 > x2) break;
+        }
+      }
+      for (int cc = 0; cc < 128; ++cc) sm.cen[rank * 129 + cc] = (double)__half2float(ri[cc]);
+    }
+    __syncthreads();
+    for (int64_t t = tid; t < Tn; t += SK_THREADS) {
+      double best = 1.0 / 0.0;
+      int b = 0;
+      for (int j = 0; j < n; ++j) {
+        double s2 = 0.0;
+        for (int cc = 0; cc < 128; ++cc) {
+          const double d = __dsub_rn((double)__half2float(X[t * 128 + cc]), sm.cen[j * 129 + cc]);
+          s2 = fma(d, d, s2);
+        }
+        if (s2 < best) { best = s2; b = j; }
+      }
+      lab[t] = b;
+    }
+    if (tid == 0) hist[0] = 0.0;
+    iters = 1;
+  } else {
+    for (int i = tid; i < k * 128; i += SK_THREADS) {
+      const int j = i >> 7, cc = i & 127;
+      sm.cen[j * 129 + cc] = (double)__half2float(X[(int64_t)chosen[j] * 128 + cc]);
+    }
+    __syncthreads();
+    int* lcur = lab;   // labels of the newest assignment
+    int* lprev = lab2; // labels the current centers were built from
+    double prev = 1.0 / 0.0;
+    for (int r = 0; r <= 25; ++r) {
+      const int mode = (r < 25 ? (SK_ASSIGN | (exact_sums ? SK_SUMS : 0)) : 0) | (r > 0 ? SK_OBJ : 0);
+      objp = 0.0;
+      sk_pass(mode, Tn, k, sm, map, row_base, ctr, nullptr, lprev, lcur, objp, bv, bi, xmax);
+      if (r > 0) {
+        const double obj = sk_block_sum(objp, sm);
+        if (tid == 0) hist[r - 1] = obj;
+        iters = r;
+        if (obj == 0.0 || (isfinite(prev) && prev - obj < 1e-6 * prev) || r == 25) {
+          fin = lprev;
+          break;
+        }
+        prev = obj;
+      }
+      // ---- empty-cluster repair of the new labels (patterns.py:112-118) -----------------
+      if (tid == 0) {
+        int ne = 0;
+        for (int j = 0; j < k; ++j) if (sm.cnt[j] == 0) sm.flags[1 + ne++] = j;
+        sm.flags[0] = ne;
+      }
+      __syncthreads();
+      const int ne = sm.flags[0];
+      bool seq = !exact_sums;
+      if (ne > 0) {
+        seq = true;
+        for (int64_t t = tid; t < Tn; t += SK_THREADS) {  // exact d2 to the assigned centers
+          const double* cj = sm.cen + lcur[t] * 129;
+          double s2 = 0.0;
+          for (int cc = 0; cc < 128; ++cc) {
+            const double d = __dsub_rn((double)__half2float(X[t * 128 + cc]), cj[cc]);
+            s2 = fma(d, d, s2);
+          }
+          own[t] = s2;
+        }
+        __syncthreads();
+        for (int ei = 0; ei < ne; ++ei) {
+          const int e = sm.flags[1 + ei];
+          double b2 = -1.0 / 0.0;
+          long long i2 = 0x7fffffffffffffffLL;
+          for (int64_t t = tid; t < Tn; t += SK_THREADS) {
+            const double v = sm.cnt[lcur[t]] > 1 ? own[t] : -1.0;
+            if (v > b2) { b2 = v; i2 = t; }
+          }
+          double fv;
+          long long far_;
+          sk_block_argmax(b2, i2, sm, fv, far_);
+          if (tid == 0) {
+            sm.cnt[lcur[far_]] -= 1;
+            sm.cnt[e] += 1;
+            lcur[far_] = e;
+            own[far_] = 0.0;
+          }
+          __syncthreads();
+        }
+      }
+      if (seq) sk_seq_sums(X, Tn, k, lcur, sm);
+      // ---- centers = means (patterns.py:119-120) ---------------------------------------
+      for (int i = tid; i < k * 128; i += SK_THREADS) {
+        const int j = i >> 7, cc = i & 127;
+        sm.cen[j * 129 + cc] = __ddiv_rn(sm.acc[i], (double)sm.cnt[j]);
+      }
+      __syncthreads();
+      int* tl = lprev; lprev = lcur; lcur = tl;
+    }
+    n = k;
+  }
+  // ---- write the pattern tables -------------------------------------------------------
+  float amax = 0.f;
+  for (int i = tid; i < n * 128; i += SK_THREADS) {
+    const int j = i >> 7, cc = i & 127;
+    const double v = sm.cen[j * 129 + cc];
+    p64[(int64_t)j * 128 + cc] = v;
+    p32[(int64_t)j * c.Dp + cc] = (float)v;
+    amax = fmaxf(amax, fabsf((float)v) * (1.f + 1e-6f));
+  }
+  for (int i = tid; i < n * (c.Dp - 128); i += SK_THREADS) {
+    const int j = i / (c.Dp - 128), cc = 128 + i % (c.Dp - 128);
+    p32[(int64_t)j * c.Dp + cc] = 0.f;
+  }
+  amax = warp_max_f(amax);
+  if ((tid & 31) == 0) sm.redv[warp] = amax;
+  __syncthreads();
+  if (tid == 0) {
+    float m = 0.f;
+    for (int w = 0; w < SK_THREADS / 32; ++w) m = fmaxf(m, (float)sm.redv[w]);
+    (side == 0 ? c.kpmax : c.vpmax)[u] = m;
+    (side == 0 ? c.nk : c.nv)[u] = n;
+    a.niter[u * 2 + side] = iters;
+  }
+  if (a.labels_out)
+    for (int64_t t = tid; t < Tn; t += SK_THREADS) a.labels_out[so + t] = fin[t];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_free<256>(*sm.tmem);
+}
+
 size_t mine_smem_bytes(int k, int D, bool tc) {
   size_t b = (size_t)k * (D + 1) * 8 + 32 * 8 + 32 * 8 + (size_t)(KMAX * 3 + 16 * KMAX + 4 + 2) * 4;
   if (tc) b += 1024 + 4 * TC_TILE * 128 + 2 * (size_t)tc_np(k) * 128 + 8 * 8 + 16 + (size_t)tc_np(k) / 2 * 4 + 64;
@@ -682,6 +1333,15 @@ cudaError_t launch_mine(const DevCache& c, const MineArgs<T>& a, cudaStream_t st
   }
   const size_t smem = mine_smem_bytes(a.k, c.D, tc);
   if constexpr (std::is_same<T, __half>::value) {
+    const char* v1 = getenv("PKV_MINE_V1");
+    if (tc && a.k <= SK_KMAX && !(v1 && v1[0] == '1') && sk_smem_bytes(a.k) <= 227 * 1024) {
+      const int s0 = (a.side_mask & 1) ? 0 : 1, ns = (a.side_mask & 1) + ((a.side_mask >> 1) & 1);
+      const size_t sb = sk_smem_bytes(a.k);
+      const cudaError_t e = cudaFuncSetAttribute(kmeans_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      if (e != cudaSuccess) return e;
+      kmeans_stream_kernel<<<c.U * ns, SK_THREADS, sb, st>>>(c, a, tk, tv, s0, ns);
+      return cudaGetLastError();
+    }
     if (tc) {
       cudaFuncSetAttribute(kmeans_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kmeans_kernel<T, true><<<dim3(c.U, 2), MINE_THREADS, smem, st>>>(c, a, tk, tv);
