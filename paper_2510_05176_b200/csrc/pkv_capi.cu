@@ -377,7 +377,7 @@ extern "C" int pkv_cache_info_get(pkv_cache* c, pkv_cache_info* o) {
 extern "C" int pkv_cache_reserve_mining(pkv_cache* c, int64_t max_tokens, void* stream) {
   if (!c) return fail(PKV_USAGE, -1, "null cache");
   if (max_tokens < 1) return fail(PKV_USAGE, -1, "max_tokens must be >= 1");
-  const size_t need = mine_scratch_need(c->U, max_tokens);
+  const size_t need = mine_scratch_need(c->U, (max_tokens + 3) / 4 * 4);
   if (need <= c->mine_scratch_bytes) return PKV_OK;
   CU(cudaStreamSynchronize((cudaStream_t)stream));
   if (c->mine_scratch) cudaFree(c->mine_scratch);
@@ -515,12 +515,13 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
   }
   int rc = reserve(c, c->dev.Tcap, std::max(c->dev.Pcap, k + 8), st);
   if (rc) return rc;
-  const size_t n2 = (size_t)U * 2 * T;
+  const int64_t Tp = (T + 3) / 4 * 4;  // scratch stride: 16-byte aligned rows per unit-side
+  const size_t n2 = (size_t)U * 2 * Tp;
   double *near_ = nullptr, *own = nullptr, *hist = nullptr;
   int *lab = nullptr, *lab2 = nullptr, *list = nullptr, *niter = nullptr;
   int64_t* first = nullptr;
   int* lab_out = nullptr;
-  const size_t need = mine_scratch_need(U, T);
+  const size_t need = mine_scratch_need(U, Tp);
   const bool own_scratch = c->mine_scratch_bytes >= need;
   unsigned char* base = c->mine_scratch;
   if (!own_scratch) CU(cudaMallocAsync((void**)&base, need, st));
@@ -547,13 +548,13 @@ static int mine_impl(pkv_cache* c, int side_mask, const void* xk, const void* xv
     a.first[0] = first; a.first[1] = first + U;
     a.k = k; a.side_mask = side_mask;
     a.near_ = near_; a.own = own; a.lab = lab; a.lab2 = lab2; a.list = list;
-    a.hist = hist; a.niter = niter; a.labels_out = lab_out;
+    a.hist = hist; a.niter = niter; a.labels_out = lab_out; a.tstride = Tp;
     return launch_mine<T_>(c->dev, a, st);
   });
   CU(e);
   if (labels_dev) {  // [U][2][T] -> the mined side's [U][T]
     const int s = (side_mask & 1) ? 0 : 1;
-    CU(cudaMemcpy2DAsync(labels_dev, (size_t)T * 4, lab_out + (size_t)s * T, (size_t)2 * T * 4, (size_t)T * 4, U,
+    CU(cudaMemcpy2DAsync(labels_dev, (size_t)T * 4, lab_out + (size_t)s * Tp, (size_t)2 * Tp * 4, (size_t)T * 4, U,
                          cudaMemcpyDeviceToDevice, st));
   }
   if (hist_host || niter_host) {
@@ -1087,6 +1088,7 @@ extern "C" int pkv_kmeans(const double* x, int64_t T, int32_t D, int32_t k, int6
   CU(cudaMallocAsync((void**)&a.hist, 2 * 25 * 8, st));
   CU(cudaMallocAsync((void**)&a.niter, 8, st));
   a.labels_out = labels;
+  a.tstride = T;
   CU(launch_mine<double>(d, a, st));
   int nc = 0, ni = 0;
   CU(cudaMemcpyAsync(&nc, d.nk, 4, cudaMemcpyDeviceToHost, st));

@@ -239,6 +239,7 @@ struct MineArgs {
   double* hist;               // [U][2][25]
   int* niter;                 // [U][2]
   int* labels_out;            // optional [U][2][T]
+  int64_t tstride;            // points per unit-side in the scratch arrays (>= T; 16-byte rows)
 };
 
 struct AttnArgs {

@@ -356,7 +356,7 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
   const int D = c.D, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t Tn = a.T;
   const T* X = a.x[side] + (int64_t)u * a.unit_stride;
-  const int64_t so = ((int64_t)u * 2 + side) * Tn;
+  const int64_t so = ((int64_t)u * 2 + side) * a.tstride;
   double* near_ = a.near_ + so;
   double* own = a.own + so;
   int* lab = a.lab + so;
@@ -662,9 +662,9 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
 // round r-1 is applied after pass r: the labels/sums pass r also produced are dropped.
 // =================================================================================
 constexpr int SK_THREADS = 384;   // warp 0 TMA, 1 MMA, 2-3 idle, 4-7 rows, 8-11 channels
-constexpr int SK_NS = 3;          // smem ring stages
+constexpr int SK_NS = 4;          // smem ring stages (even: split seeding gives each consumer group its own stages)
 constexpr int SK_ROW0 = 4, SK_CH0 = 8;
-constexpr int SK_KMAX = 48;
+constexpr int SK_KMAX = 32;
 
 struct SkSmem {
   unsigned char* sA;   // [NS][2 halves][128 rows x 128 B] swizzled fp16 tiles
@@ -672,6 +672,9 @@ struct SkSmem {
   double* cen;         // [k][129]
   double* acc;         // [k][128] centroid sums
   double* seed;        // [128] newest seed row (fp64)
+  float* seed32;       // [128] the same row in fp32 (exact: fp16 values)
+  double* sNear;       // [NS][128] running seeding minima of the tile's points (bulk-loaded)
+  int* sLab;           // [NS][128] previous labels of the tile's points (bulk-loaded)
   int* labs;           // [NS][128] labels of the tile's rows (row -> channel warps)
   float* cc;           // [NP/2]
   int* cnt;            // [k]
@@ -684,66 +687,111 @@ struct SkSmem {
 };
 __host__ __device__ inline size_t sk_smem_bytes(int k) {
   const int NP = ((2 * k + 15) / 16) * 16;
-  return 1024 + (size_t)SK_NS * 2 * 16384 + 2 * (size_t)NP * 128 + (size_t)k * 129 * 8 + (size_t)k * 128 * 8 + 128 * 8 +
+  return 1024 + (size_t)SK_NS * 2 * 16384 + 2 * (size_t)NP * 128 + (size_t)k * 129 * 8 + (size_t)k * 128 * 8 + 128 * 12 +
+         SK_NS * 128 * 12 +
          SK_NS * 128 * 4 + (size_t)NP / 2 * 4 + 2 * (size_t)k * 4 + 8 * 4 + 16 * 8 + 16 * 8 + (3 * SK_NS + 4) * 8 + 16 + 64 +
          14 * 16;  // 16-byte carve alignment
 }
 __device__ __forceinline__ unsigned char* sk_tile(const SkSmem& s, int stage, int half) {
   return s.sA + (stage * 2 + half) * 16384;
 }
-#define SK_SMEM(p) __builtin_assume(__isShared(p))
-__device__ __forceinline__ double h2d(__half h) {  // one F2F.F64.F16
+using sm100::smem_u32;
+// explicit shared-space loads on 32-bit addresses (no generic->shared conversions in the
+// hot loops); volatile keeps them ordered against the mbarrier waits
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double ldsd(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void stsd(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+__device__ __forceinline__ unsigned short lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double h2d_bits(unsigned short h) {  // one F2F.F64.F16
   double r;
-  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(__half_as_ushort(h)));
+  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(h));
   return r;
 }
-// fp64 squared distance of tile row `row` to a fp64 row `cj`, channel order, one fma
-// chain (the v1 arithmetic; used for the near-tie label decisions)
-__device__ __forceinline__ double sk_d2(const unsigned char* tile, int row, const double* cj) {
-  SK_SMEM(tile); SK_SMEM(cj);
+__device__ __forceinline__ double h2d(__half h) { return h2d_bits(__half_as_ushort(h)); }
+// shared address of 16-byte chunk q (channels 8q .. 8q+7) of row `row` of a swizzled tile
+__device__ __forceinline__ uint32_t sk_chunk(uint32_t tile_s, int row, int q) {
+  return tile_s + (q >> 3) * 16384 + row * 128 + ((((q & 7) ^ (row & 7))) << 4);
+}
+// fp64 squared distance of tile row `row` to a fp64 row at cj_s, channel order, one fma
+// chain (the v1 arithmetic)
+__device__ __forceinline__ double sk_d2(uint32_t tile_s, int row, uint32_t cj_s) {
   double a0 = 0.0;
+#pragma unroll 2
+  for (int q = 0; q < 16; ++q) {
+    const uint4 v = lds128(sk_chunk(tile_s, row, q));
+    const __half* h = reinterpret_cast<const __half*>(&v);
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const unsigned char* base = tile + half * 16384 + row * 128;
-#pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-      const uint4 v = *reinterpret_cast<const uint4*>(base + ((ch ^ (row & 7)) << 4));
-      const __half* h = reinterpret_cast<const __half*>(&v);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const double d = __dsub_rn(h2d(h[e]), cj[half * 64 + ch * 8 + e]);
-        a0 = fma(d, d, a0);
-      }
+    for (int e = 0; e < 8; ++e) {
+      const double d = __dsub_rn(h2d(h[e]), ldsd(cj_s + 8 * (8 * q + e)));
+      a0 = fma(d, d, a0);
     }
   }
   return a0;
 }
 // the same distance with four independent accumulators (a 32-deep instead of a 128-deep
-// dependency chain: seeding minima and the objective); |x|max of the row on request
+// dependency chain: seeding minima, the objective, near-tie candidates); |x|max on request
 template <bool XMAX>
-__device__ __forceinline__ double sk_d2x4(const unsigned char* tile, int row, const double* cj, float* xmax) {
-  SK_SMEM(tile); SK_SMEM(cj);
+__device__ __forceinline__ double sk_d2x4(uint32_t tile_s, int row, uint32_t cj_s, float* xmax) {
   double a[4] = {0.0, 0.0, 0.0, 0.0};
   float xm = 0.f;
 #pragma unroll 4
-  for (int q = 0; q < 16; ++q) {  // 16-byte chunk q = channels 8q .. 8q+7
-    const int half = q >> 3, ch = q & 7;
-    const uint4 v = *reinterpret_cast<const uint4*>(tile + half * 16384 + row * 128 + ((ch ^ (row & 7)) << 4));
+  for (int q = 0; q < 16; ++q) {
+    const uint4 v = lds128(sk_chunk(tile_s, row, q));
     const __half* h = reinterpret_cast<const __half*>(&v);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       if (XMAX) xm = fmaxf(xm, fabsf(__half2float(h[e])));
-      const double d = __dsub_rn(h2d(h[e]), cj[8 * q + e]);
+      const double d = __dsub_rn(h2d(h[e]), ldsd(cj_s + 8 * (8 * q + e)));
       a[e & 3] = fma(d, d, a[e & 3]);
     }
   }
   if (XMAX) *xmax = fmaxf(*xmax, xm);
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
+// fp32 squared distance of tile row `row` to the fp32 seed row, four partial sums:
+// |d2_32 - d2| <= 2^-18 d2 (x and the seed are fp16 values, exact in fp32; one rounding
+// per difference, <= 34 roundings per partial-sum chain), so d2_32 (1 - 2^-16) is a
+// lower bound of the exact distance
+__device__ __forceinline__ float sk_d2_f32(uint32_t tile_s, int row, uint32_t s32_s) {
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int q = 0; q < 16; ++q) {
+    const uint4 v = lds128(sk_chunk(tile_s, row, q));
+    const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+    const uint4 sa = lds128(s32_s + 32 * q), sb = lds128(s32_s + 32 * q + 16);
+    const float sv[8] = {__uint_as_float(sa.x), __uint_as_float(sa.y), __uint_as_float(sa.z), __uint_as_float(sa.w),
+                         __uint_as_float(sb.x), __uint_as_float(sb.y), __uint_as_float(sb.z), __uint_as_float(sb.w)};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(h2[e]);
+      const float d0 = f.x - sv[2 * e], d1 = f.y - sv[2 * e + 1];
+      a[e] = fmaf(d0, d0, a[e]);
+      a[e] = fmaf(d1, d1, a[e]);
+    }
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
 
 struct SkCounters { uint32_t gt, gm, gl; };  // tiles streamed, MMA tiles, label hand-offs
 
-enum { SK_SEED = 1, SK_ASSIGN = 2, SK_OBJ = 4, SK_SUMS = 8, SK_FIRST = 16 };
+enum { SK_SEED = 1, SK_ASSIGN = 2, SK_OBJ = 4, SK_SUMS = 8, SK_FIRST = 16, SK_SPLIT = 32 };
 
 // Block reductions over the 8 consumer warps (rows 4-7 carry the values; others pass identity)
 __device__ __forceinline__ double sk_block_sum(double v, const SkSmem& sm) {
@@ -770,6 +818,29 @@ __device__ __forceinline__ void sk_block_argmax(double v, long long i, const SkS
     if (v2 > ov || (v2 == ov && i2 < oi)) { ov = v2; oi = i2; }
   }
   __syncthreads();
+}
+
+// Split seeding: the row warps take the even tiles and the channel warps the odd ones.
+// With an even stage count each group owns its stages, so no group ever skips a phase of
+// a stage's mbarrier (a skipped phase would make the parity test ambiguous).
+// Seeding update of one tile row: running minimum of the fp64 squared distances to the
+// chosen seeds (exact fp64 only where the newest seed can lower it), argmax tracking.
+__device__ __forceinline__ void sk_seed_row(const SkSmem& sm, uint32_t tile_s, int s, int row, int64_t t, int mode,
+                                            double* near_, double& bv, long long& bi_out, float& xmax) {
+  const uint32_t seed_s = smem_u32(sm.seed);
+  double nv;
+  if (mode & SK_FIRST) {
+    nv = sk_d2x4<true>(tile_s, row, seed_s, &xmax);
+    near_[t] = nv;
+  } else {
+    nv = sm.sNear[s * 128 + row];
+    const float lb = sk_d2_f32(tile_s, row, smem_u32(sm.seed32)) * 0.9999847412109375f;  // (1 - 2^-16)
+    if ((double)lb < nv) {
+      const double d = sk_d2x4<false>(tile_s, row, seed_s, nullptr);
+      if (d < nv) { nv = d; near_[t] = nv; }
+    }
+  }
+  if (nv > bv) { bv = nv; bi_out = t; }
 }
 
 // One streamed pass.  Returns, on row threads, this thread's share of the objective
@@ -821,13 +892,20 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
 
   if (warp == 0) {
     if (lane == 0) {
+      const bool ld_near = (mode & SK_SEED) && !(mode & SK_FIRST), ld_lab = mode & SK_OBJ;
       for (int m = 0; m < NT; ++m) {
         const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], 2 * 16384);
+        const int rows = (int)min((int64_t)128, Tn - (int64_t)m * 128);
+        const uint32_t nb_near = ld_near ? (uint32_t)((rows * 8 + 15) & ~15) : 0u;
+        const uint32_t nb_lab = ld_lab ? (uint32_t)((rows * 4 + 15) & ~15) : 0u;
+        mbar_wait_sleep(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], 2 * 16384 + nb_near + nb_lab);
         const int r0 = (int)(row_base + (int64_t)m * 128);
         tma_load_2d(sk_tile(sm, s, 0), map, &full[s], 0, r0);
         tma_load_2d(sk_tile(sm, s, 1), map, &full[s], 64, r0);
+        // per-point state rides with the tile (no global load on the consumers' path)
+        if (nb_near) bulk_load(sm.sNear + s * 128, near_ + (int64_t)m * 128, nb_near, &full[s]);
+        if (nb_lab) bulk_load(sm.sLab + s * 128, lab_old + (int64_t)m * 128, nb_lab, &full[s]);
       }
     }
     __syncwarp();
@@ -838,8 +916,8 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
       for (int m = 0; m < NT; ++m) {
         const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
         const uint32_t gm = ctr.gm + m, acc = gm & 1, aph = (gm >> 1) & 1;
-        mbar_wait(&full[s], ph);
-        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait_sleep(&full[s], ph);
+        mbar_wait_sleep(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint64_t da0 = smem_desc_k_sw128(sk_tile(sm, s, 0)), da1 = smem_desc_k_sw128(sk_tile(sm, s, 1));
 #pragma unroll
@@ -858,14 +936,17 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
     if (assign)
       for (int j = 0; j < k; ++j) ccmax = fmaxf(ccmax, sm.cc[j]);
     const float cnorm = sqrtf(ccmax);
-    for (int m = 0; m < NT; ++m) {
+    const uint32_t cc_s = smem_u32(sm.cc);
+    const bool seedp = mode & SK_SEED, split = seedp && (mode & SK_SPLIT);
+    for (int m = 0; m < NT; m += split ? 2 : 1) {  // split seeding: even tiles (channel warps: odd)
       const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
       const int64_t t = (int64_t)m * 128 + row;
       const bool live = t < Tn;
       const unsigned char* tile = sk_tile(sm, s, 0);
+      const uint32_t tile_s = smem_u32(tile);
       int bi = 0;
       float vb = __int_as_float(0x7f800000), vs = vb;
-      mbar_wait(&full[s], ph);
+      mbar_wait_sleep(&full[s], ph);
       if (assign) {
         const uint32_t gm = ctr.gm + m, acc = gm & 1, aph = (gm >> 1) & 1;
         const uint32_t tbase = *sm.tmem + acc * 128 + ((uint32_t)(32 * q) << 16);
@@ -873,11 +954,9 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
         float xq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          const unsigned char* base = tile + half * 16384 + row * 128;
-          SK_SMEM(base);
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch) {
-            const uint4 w = *reinterpret_cast<const uint4*>(base + ((ch ^ (row & 7)) << 4));
+            const uint4 w = lds128(sk_chunk(tile_s, row, 8 * half + ch));
             const __half2* h2 = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -889,7 +968,7 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
         const float xx = (xq[0] + xq[1]) + (xq[2] + xq[3]);
         // same error bound as the v1 tensor-core pass (K2)
         const float tol = 1.52587890625e-05f * sqrtf(xx) * cnorm + 4.76837158203125e-07f * (ccmax + xx);
-        mbar_wait(&tfull[acc], aph);
+        mbar_wait_sleep(&tfull[acc], aph);
         tc_fence_after();
 #pragma unroll 1
         for (int c0 = 0; c0 < NP; c0 += 16) {
@@ -901,7 +980,7 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
             const int j = c0 / 2 + e;
             if (j < k) {
               const float dot = __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]);
-              const float val = fmaf(-2.f, dot, sm.cc[j]);
+              const float val = fmaf(-2.f, dot, ldsf(cc_s + 4 * j));
               if (val < vb) { vs = vb; vb = val; bi = j; }
               else vs = fminf(vs, val);
             }
@@ -923,14 +1002,14 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int j = c0 / 2 + e;
-              if (j < k && fmaf(-2.f, __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]), sm.cc[j]) <= lim)
+              if (j < k && fmaf(-2.f, __uint_as_float(v[2 * e]) + __uint_as_float(v[2 * e + 1]), ldsf(cc_s + 4 * j)) <= lim)
                 cand |= 1u << e;
             }
             if (!tie) cand = 0u;
             while (cand) {
               const int j = c0 / 2 + __ffs(cand) - 1;
               cand &= cand - 1;
-              const double d = sk_d2x4<false>(tile, row, sm.cen + j * 129, nullptr);
+              const double d = sk_d2x4<false>(tile_s, row, smem_u32(sm.cen + j * 129), nullptr);
               if (d < best) { best = d; bj = j; }
             }
           }
@@ -940,25 +1019,21 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
         mbar_arrive(&tempty[acc]);
       }
       if (live) {
-        if (mode & SK_SEED) {
-          const double d = (mode & SK_FIRST) ? sk_d2x4<true>(tile, row, sm.seed, &xmax)
-                                             : sk_d2x4<false>(tile, row, sm.seed, nullptr);
-          const double nv = (mode & SK_FIRST) ? d : fmin(near_[t], d);
-          near_[t] = nv;
-          if (nv > bv) { bv = nv; bi_out = t; }
-        }
+        if (seedp) sk_seed_row(sm, tile_s, s, row, t, mode, near_, bv, bi_out, xmax);
         if (assign) {
           lab_new[t] = bi;
           atomicAdd(&sm.cnt[bi], 1);
         }
-        if (mode & SK_OBJ) obj += sk_d2x4<false>(tile, row, sm.cen + lab_old[t] * 129, nullptr);
+        if (mode & SK_OBJ) obj += sk_d2x4<false>(tile_s, row, smem_u32(sm.cen + sm.sLab[s * 128 + row] * 129), nullptr);
       }
+
       if (sums) {  // label hand-off slot/barrier follow their own counter (gl), not the tile stage
         const uint32_t ls = (ctr.gl + m) % SK_NS;
         sm.labs[ls * 128 + row] = live ? bi : -1;
         mbar_arrive(&lready[ls]);
       }
-      mbar_arrive(&empty[s]);
+      if (split) mbar_arrive_cnt(&empty[s], 2);  // this group alone consumed the tile
+      else mbar_arrive(&empty[s]);
     }
   } else if (warp >= SK_CH0 && warp < SK_CH0 + 4) {
     const int c = tid - 32 * SK_CH0;  // channel
@@ -967,24 +1042,23 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
       const uint32_t g = ctr.gt + m, s = g % SK_NS, ph = (g / SK_NS) & 1;
       if (sums) {
         const uint32_t gl = ctr.gl + m, ls = gl % SK_NS, lph = (gl / SK_NS) & 1;
-        mbar_wait(&lready[ls], lph);
-        const unsigned char* tile = sk_tile(sm, s, 0) + hoff;
-        const int* lb = sm.labs + ls * 128;
-        double* accc = sm.acc + c;
-        SK_SMEM(tile); SK_SMEM(lb); SK_SMEM(accc);
+        mbar_wait_sleep(&lready[ls], lph);
+        const uint32_t tile_s = smem_u32(sk_tile(sm, s, 0)) + hoff;
+        const uint32_t lb_s = smem_u32(sm.labs + ls * 128);
+        const uint32_t acc_s = smem_u32(sm.acc + c);
         // rows in blocks of 8: labels and values load up front; the current label's run is
         // summed in two interleaved registers (exact sums: any order) and flushed on a change
         int curj = -1;
         double run0 = -0.0, run1 = -0.0;
         for (int r0 = 0; r0 < 128; r0 += 8) {
-          const int4 la = *reinterpret_cast<const int4*>(lb + r0);
-          const int4 lb4 = *reinterpret_cast<const int4*>(lb + r0 + 4);
-          const int js[8] = {la.x, la.y, la.z, la.w, lb4.x, lb4.y, lb4.z, lb4.w};
+          const uint4 la = lds128(lb_s + 4 * r0);
+          const uint4 lb4 = lds128(lb_s + 4 * r0 + 16);
+          const int js[8] = {(int)la.x, (int)la.y, (int)la.z, (int)la.w, (int)lb4.x, (int)lb4.y, (int)lb4.z, (int)lb4.w};
           double xs[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int r = r0 + e;
-            xs[e] = h2d(*reinterpret_cast<const __half*>(tile + r * 128 + ((cb ^ (r & 7)) << 4)));
+            xs[e] = h2d_bits(lds16(tile_s + r * 128 + ((cb ^ (r & 7)) << 4)));
           }
           bool same = curj >= 0;
 #pragma unroll
@@ -999,7 +1073,7 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
             const int j = js[e];
             if (j < 0) continue;  // past Tn
             if (j != curj) {
-              if (curj >= 0) accc[curj * 128] = __dadd_rn(accc[curj * 128], __dadd_rn(run0, run1));
+              if (curj >= 0) stsd(acc_s + curj * 1024, __dadd_rn(ldsd(acc_s + curj * 1024), __dadd_rn(run0, run1)));
               curj = j;
               run0 = xs[e];
               run1 = -0.0;
@@ -1010,9 +1084,17 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
             }
           }
         }
-        if (curj >= 0) accc[curj * 128] = __dadd_rn(accc[curj * 128], __dadd_rn(run0, run1));
+        if (curj >= 0) stsd(acc_s + curj * 1024, __dadd_rn(ldsd(acc_s + curj * 1024), __dadd_rn(run0, run1)));
+      } else if ((mode & SK_SEED) && (mode & SK_SPLIT)) {  // seeding: the odd tiles (row warps: even)
+        if (m & 1) {
+          mbar_wait_sleep(&full[s], ph);
+          const int64_t t = (int64_t)m * 128 + c;
+          if (t < Tn) sk_seed_row(sm, smem_u32(sk_tile(sm, s, 0)), s, c, t, mode, near_, bv, bi_out, xmax);
+          mbar_arrive_cnt(&empty[s], 2);
+        }
+        continue;
       } else {
-        mbar_wait(&full[s], ph);
+        mbar_wait_sleep(&full[s], ph);
       }
       mbar_arrive(&empty[s]);
     }
@@ -1020,6 +1102,7 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
   ctr.gt += NT;
   if (assign) ctr.gm += NT;
   if (sums) ctr.gl += NT;
+  fence_proxy_async_global();  // near_/labels written here are bulk-read (async proxy) next pass
   __syncthreads();
 }
 
@@ -1059,7 +1142,7 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
   const int k = a.k, tid = threadIdx.x, warp = tid >> 5;
   const int64_t Tn = a.T;
   const __half* X = a.x[side] + (int64_t)u * a.unit_stride;
-  const int64_t so = ((int64_t)u * 2 + side) * Tn;
+  const int64_t so = ((int64_t)u * 2 + side) * a.tstride;
   double* near_ = a.near_ + so;
   double* own = a.own + so;
   int* lab = a.lab + so;
@@ -1082,6 +1165,9 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
     sm.cen = reinterpret_cast<double*>(carve((size_t)k * 129 * 8));
     sm.acc = reinterpret_cast<double*>(carve((size_t)k * 128 * 8));
     sm.seed = reinterpret_cast<double*>(carve(128 * 8));
+    sm.seed32 = reinterpret_cast<float*>(carve(128 * 4));
+    sm.sNear = reinterpret_cast<double*>(carve(SK_NS * 128 * 8));
+    sm.sLab = reinterpret_cast<int*>(carve(SK_NS * 128 * 4));
     sm.redv = reinterpret_cast<double*>(carve(16 * 8));
     sm.redi = reinterpret_cast<long long*>(carve(16 * 8));
     sm.bars = reinterpret_cast<uint64_t*>(carve((3 * SK_NS + 4) * 8));
@@ -1119,9 +1205,13 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
   const int64_t first = a.first[side][u];
   int* chosen = sm.off;  // seed indices (k)
   if (tid == 0) chosen[0] = (int)first;
-  for (int c2 = tid; c2 < 128; c2 += SK_THREADS) sm.seed[c2] = (double)__half2float(X[first * 128 + c2]);
+  for (int c2 = tid; c2 < 128; c2 += SK_THREADS) {
+    sm.seed32[c2] = __half2float(X[first * 128 + c2]);
+    sm.seed[c2] = (double)sm.seed32[c2];
+  }
   __syncthreads();
-  sk_pass(SK_SEED | SK_FIRST, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
+  const int split = (a.side_mask & 4) ? 0 : SK_SPLIT;  // bit 2: debugging switch (one consumer group)
+  sk_pass(SK_SEED | SK_FIRST | split, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
   double vmax;
   long long imax;
   sk_block_argmax(bv, bi, sm, vmax, imax);
@@ -1143,11 +1233,14 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
     if (n == k) break;
     if (tid == 0) chosen[n] = (int)imax;
     ++n;
-    for (int c2 = tid; c2 < 128; c2 += SK_THREADS) sm.seed[c2] = (double)__half2float(X[imax * 128 + c2]);
+    for (int c2 = tid; c2 < 128; c2 += SK_THREADS) {
+      sm.seed32[c2] = __half2float(X[imax * 128 + c2]);
+      sm.seed[c2] = (double)sm.seed32[c2];
+    }
     __syncthreads();
     bv = -1.0 / 0.0;
     bi = 0x7fffffffffffffffLL;
-    sk_pass(SK_SEED, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
+    sk_pass(SK_SEED | split, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
     sk_block_argmax(bv, bi, sm, vmax, imax);
   }
 
@@ -1245,6 +1338,7 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
             sm.cnt[e] += 1;
             lcur[far_] = e;
             own[far_] = 0.0;
+            sm100::fence_proxy_async_global();  // lcur is bulk-read (async proxy) by the next pass
           }
           __syncthreads();
         }
@@ -1336,10 +1430,13 @@ cudaError_t launch_mine(const DevCache& c, const MineArgs<T>& a, cudaStream_t st
     const char* v1 = getenv("PKV_MINE_V1");
     if (tc && a.k <= SK_KMAX && !(v1 && v1[0] == '1') && sk_smem_bytes(a.k) <= 227 * 1024) {
       const int s0 = (a.side_mask & 1) ? 0 : 1, ns = (a.side_mask & 1) + ((a.side_mask >> 1) & 1);
+      const char* ns1 = getenv("PKV_MINE_NOSPLIT");
+      MineArgs<__half> a2 = a;
+      if (ns1 && ns1[0] == '1') a2.side_mask |= 4;
       const size_t sb = sk_smem_bytes(a.k);
       const cudaError_t e = cudaFuncSetAttribute(kmeans_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
       if (e != cudaSuccess) return e;
-      kmeans_stream_kernel<<<c.U * ns, SK_THREADS, sb, st>>>(c, a, tk, tv, s0, ns);
+      kmeans_stream_kernel<<<c.U * ns, SK_THREADS, sb, st>>>(c, a2, tk, tv, s0, ns);
       return cudaGetLastError();
     }
     if (tc) {
