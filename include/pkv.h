@@ -196,6 +196,14 @@ int pkv_cache_read(pkv_cache* c, const char* name, int64_t offset, int64_t n, vo
  * offsets[n+1] (device), outputs scale/zero [n] and unpacked codes. */
 int pkv_quantize_groups(const double* values, const int64_t* offsets, int32_t n, int32_t bits, double* scale,
                         double* zero, uint8_t* codes, void* stream);
+/* quantize_group (quant.py:70-111) + pack_codes (quant.py:120-146) of ONE group of n
+ * host values: host outputs scale, zero and ceil(n*bits/8) packed bytes (the reference's
+ * byte layout).  Non-finite value -> PKV_DATA with its index.  Synchronous. */
+int pkv_quantize_group_host(const double* values, int64_t n, int32_t bits, double* scale, double* zero,
+                            uint8_t* packed);
+/* dequantize_group (quant.py:114-117): scale * code + zero in IEEE fp64 for n codes packed
+ * in host memory -> host out[n].  Synchronous. */
+int pkv_dequantize_group_host(const uint8_t* packed, int64_t n, int32_t bits, double scale, double zero, double* out);
 /* pack_codes / unpack_codes (quant.py:120-179) on device buffers */
 int pkv_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out, void* stream);
 int pkv_unpack_codes(const uint8_t* packed, int64_t n, int32_t bits, uint8_t* codes, void* stream);

@@ -77,6 +77,8 @@ PROTOTYPES = {
     "pkv_cache_buffer": (C.c_int, [_vp, C.c_char_p, _P(_vp), _P(_i64)]),
     "pkv_cache_read": (C.c_int, [_vp, C.c_char_p, _i64, _i64, _vp, _vp]),
     "pkv_quantize_groups": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "pkv_quantize_group_host": (C.c_int, [_vp, _i64, _i32, _P(_f64), _P(_f64), _vp]),
+    "pkv_dequantize_group_host": (C.c_int, [_vp, _i64, _i32, _f64, _f64, _vp]),
     "pkv_pack_codes": (C.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "pkv_unpack_codes": (C.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "pkv_match": (C.c_int, [_vp, _i64, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),

@@ -141,6 +141,9 @@ class KvStream:
             setattr(self, name, arr)
         if self.prefill_k.shape != self.prefill_v.shape or self.decode_k.shape != self.decode_v.shape:
             raise UsageError("K and V tensors must have matching shapes")
+        pk, dk = self.prefill_k.shape, self.decode_k.shape
+        if (dk[0], dk[1], dk[3]) != (pk[0], pk[1], pk[3]):
+            raise UsageError("decode tensors must match prefill layers/heads/dim")
         if self.prefill_k.shape[2] < 1:
             raise UsageError("prefill length must be >= 1")
 

@@ -1032,6 +1032,83 @@ extern "C" int pkv_quantize_groups(const double* values, const int64_t* offsets,
   CU(launch_quantize_groups(values, offsets, n, bits, scale, zero, codes, (cudaStream_t)stream));
   return PKV_OK;
 }
+// single-group host API: a per-thread pinned staging buffer + device buffer + stream, one
+// H2D, one kernel, one D2H per call (the reference's per-group functions are called in loops)
+struct GroupCtx {
+  cudaStream_t st = nullptr;
+  unsigned char* host = nullptr;
+  unsigned char* dev = nullptr;
+  size_t cap = 0;
+  ~GroupCtx() {
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+static thread_local GroupCtx g_group;
+static int group_ctx(size_t bytes) {
+  GroupCtx& g = g_group;
+  if (!g.st) CU(cudaStreamCreateWithFlags(&g.st, cudaStreamNonBlocking));
+  if (bytes > g.cap) {
+    if (g.host) cudaFreeHost(g.host);
+    if (g.dev) cudaFree(g.dev);
+    g.host = nullptr; g.dev = nullptr; g.cap = 0;
+    const size_t cap = std::max<size_t>(bytes, 64 * 1024);
+    CU(cudaHostAlloc((void**)&g.host, cap, cudaHostAllocDefault));
+    CU(cudaMalloc((void**)&g.dev, cap));
+    g.cap = cap;
+  }
+  return PKV_OK;
+}
+
+extern "C" int pkv_quantize_group_host(const double* values, int64_t n, int32_t bits, double* scale, double* zero,
+                                       uint8_t* packed) {
+  if (bits != 2 && bits != 4 && bits != 8)
+    return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", bits);
+  if (n < 1) return fail(PKV_USAGE, -1, "cannot quantize an empty group");
+  if (!values || !scale || !zero || !packed) return fail(PKV_USAGE, -1, "null argument");
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(values[i])) return fail(PKV_DATA, i, "non-finite value at index %lld: %g", (long long)i, values[i]);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PKV_USAGE, -1, "no CUDA device: the PatternKV B200 codec has no CPU fallback");
+  const size_t nb = (size_t)(n * bits + 7) / 8, vb = (size_t)n * 8, ob = 16 + ((nb + 15) & ~(size_t)15);
+  int rc = group_ctx(vb + ob);
+  if (rc) return rc;
+  GroupCtx& g = g_group;
+  std::memcpy(g.host, values, vb);
+  CU(cudaMemcpyAsync(g.dev, g.host, vb, cudaMemcpyHostToDevice, g.st));
+  CU(launch_qpack((const double*)g.dev, n, bits, (double*)(g.dev + vb), g.dev + vb + 16, g.st));
+  CU(cudaMemcpyAsync(g.host + vb, g.dev + vb, 16 + nb, cudaMemcpyDeviceToHost, g.st));
+  CU(cudaStreamSynchronize(g.st));
+  std::memcpy(scale, g.host + vb, 8);
+  std::memcpy(zero, g.host + vb + 8, 8);
+  std::memcpy(packed, g.host + vb + 16, nb);
+  return PKV_OK;
+}
+
+extern "C" int pkv_dequantize_group_host(const uint8_t* packed, int64_t n, int32_t bits, double scale, double zero,
+                                         double* out) {
+  if (bits != 2 && bits != 4 && bits != 8)
+    return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", bits);
+  if (n < 0 || (n > 0 && (!packed || !out))) return fail(PKV_USAGE, -1, "null argument");
+  if (n == 0) return PKV_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PKV_USAGE, -1, "no CUDA device: the PatternKV B200 codec has no CPU fallback");
+  const size_t nb = (size_t)(n * bits + 7) / 8, pb = (nb + 15) & ~(size_t)15, ob = (size_t)n * 8;
+  int rc = group_ctx(pb + ob);
+  if (rc) return rc;
+  GroupCtx& g = g_group;
+  std::memcpy(g.host, packed, nb);
+  CU(cudaMemcpyAsync(g.dev, g.host, nb, cudaMemcpyHostToDevice, g.st));
+  CU(launch_dqunpack(g.dev, n, bits, scale, zero, (double*)(g.dev + pb), g.st));
+  CU(cudaMemcpyAsync(g.host + pb, g.dev + pb, ob, cudaMemcpyDeviceToHost, g.st));
+  CU(cudaStreamSynchronize(g.st));
+  std::memcpy(out, g.host + pb, ob);
+  return PKV_OK;
+}
+
 extern "C" int pkv_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out, void* stream) {
   if (bits != 2 && bits != 4 && bits != 8)
     return fail(PKV_USAGE, -1, "unsupported bit width %d; expected one of (2, 4, 8)", bits);

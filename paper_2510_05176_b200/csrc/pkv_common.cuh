@@ -273,6 +273,8 @@ cudaError_t launch_fork(const ForkArenas&, int, const int*, const int*, cudaStre
 cudaError_t launch_codes(const DevCache&, int, int64_t, int64_t, uint8_t*, uint8_t*, cudaStream_t);
 cudaError_t launch_quantize_groups(const double*, const int64_t*, int, int, double*, double*, uint8_t*, cudaStream_t);
 cudaError_t launch_pack(const uint8_t*, int64_t, int, uint8_t*, cudaStream_t);
+cudaError_t launch_qpack(const double*, int64_t, int, double*, uint8_t*, cudaStream_t);
+cudaError_t launch_dqunpack(const uint8_t*, int64_t, int, double, double, double*, cudaStream_t);
 cudaError_t launch_unpack(const uint8_t*, int64_t, int, uint8_t*, cudaStream_t);
 cudaError_t launch_match(const double*, int64_t, const double*, int, int, int64_t*, double*, double*, cudaStream_t);
 cudaError_t launch_midrange(const double*, int64_t, int, double*, cudaStream_t);

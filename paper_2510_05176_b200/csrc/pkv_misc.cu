@@ -443,3 +443,51 @@ cudaError_t launch_fork(const ForkArenas& fa, int n, const int* src, const int* 
 }
 
 }  // namespace pkv
+
+namespace pkv {
+
+// ---- single-group quantize+pack / unpack+dequantize (quant.py:70-179) -------------------
+// One CTA: block min/max, the exact code rule of quant_code, the packed bytes straight out.
+__global__ void qpack_kernel(const double* v, int64_t n, int bits, double* sz, uint8_t* packed) {
+  __shared__ double rmin[32], rmax[32];
+  double lo = 1.0 / 0.0, hi = -1.0 / 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) { lo = fmin(lo, v[i]); hi = fmax(hi, v[i]); }
+  lo = warp_min_d(lo);
+  hi = warp_max_d(hi);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) { rmin[warp] = lo; rmax[warp] = hi; }
+  __syncthreads();
+  lo = rmin[0]; hi = rmax[0];
+  for (int w = 1; w < nw; ++w) { lo = fmin(lo, rmin[w]); hi = fmax(hi, rmax[w]); }
+  const QuantParamsDev qp = make_qparams(lo, hi, (1 << bits) - 1);
+  const int per = 8 / bits;
+  const int64_t nb = (n + per - 1) / per;
+  for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    unsigned byte = 0;
+    for (int k = 0; k < per; ++k) {
+      const int64_t j = b * per + k;
+      if (j < n) byte |= (unsigned)quant_code(v[j], qp, nullptr) << (k * bits);
+    }
+    packed[b] = (uint8_t)byte;
+  }
+  if (threadIdx.x == 0) { sz[0] = qp.scale; sz[1] = qp.lo; }
+}
+__global__ void dqunpack_kernel(const uint8_t* packed, int64_t n, int bits, double scale, double zero, double* out) {
+  const int per = 8 / bits;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int code = (packed[j / per] >> ((j % per) * bits)) & ((1 << bits) - 1);
+    out[j] = __dadd_rn(__dmul_rn(scale, (double)code), zero);
+  }
+}
+cudaError_t launch_qpack(const double* v, int64_t n, int bits, double* sz, uint8_t* packed, cudaStream_t st) {
+  qpack_kernel<<<1, 256, 0, st>>>(v, n, bits, sz, packed);
+  return cudaGetLastError();
+}
+cudaError_t launch_dqunpack(const uint8_t* packed, int64_t n, int bits, double scale, double zero, double* out,
+                            cudaStream_t st) {
+  const int g = (int)imin64((n + 255) / 256, 1024);
+  dqunpack_kernel<<<g, 256, 0, st>>>(packed, n, bits, scale, zero, out);
+  return cudaGetLastError();
+}
+
+}  // namespace pkv

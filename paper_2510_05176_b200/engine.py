@@ -187,6 +187,7 @@ def prefill(k_tensor, v_tensor, config: EngineConfig) -> HeadCacheState:
 
 def append_decode_token(k_vec, v_vec, state: HeadCacheState) -> HeadCacheState:
     """Append one token; flush the oldest group when the window reaches W + G (engine.py:172-198)."""
+    state = _on_device(state)
     k = np.asarray(k_vec, dtype=np.float64).ravel()
     v = np.asarray(v_vec, dtype=np.float64).ravel()
     if k.shape != (state.head_dim,) or v.shape != (state.head_dim,):
@@ -197,8 +198,14 @@ def append_decode_token(k_vec, v_vec, state: HeadCacheState) -> HeadCacheState:
     return state
 
 
+def _on_device(state):
+    """A HeadCacheState as is; a loaded snapshot state (snapshot.SnapshotState) resumed on the GPU."""
+    return state if isinstance(state, HeadCacheState) else state.device_state()
+
+
 def reconstruct_token(state: HeadCacheState, token_index: int) -> tuple[np.ndarray, np.ndarray]:
     """One token's (K, V); exact for window tokens (engine.py:271-293)."""
+    state = _on_device(state)
     if not 0 <= token_index < state.token_count:
         raise UsageError(f"token index {token_index} outside [0, {state.token_count})")
     committed = state.committed_count
@@ -212,6 +219,7 @@ def reconstruct_token(state: HeadCacheState, token_index: int) -> tuple[np.ndarr
 
 def committed_matrices(state: HeadCacheState) -> tuple[np.ndarray, np.ndarray]:
     """All committed tokens reconstructed (engine.py:296-303), exact fp64 on the GPU."""
+    state = _on_device(state)
     d = state.head_dim
     if state.committed_count == 0:
         return np.empty((0, d)), np.empty((0, d))

@@ -82,17 +82,30 @@ def quantize_group(values: np.ndarray, bits: int, layout: str = PER_TOKEN) -> Qu
     if not finite.all():
         idx = int(np.flatnonzero(~finite)[0])
         raise DataError(f"non-finite value at index {idx}: {vals[idx]}")
-    scale, zero, codes = quantize_groups([vals], bits)[0]
-    return QuantizedGroup(params=QuantParams(scale=scale, zero_point=zero, bits=bits),
-                          codes=pack_codes(codes, bits), length=vals.size, layout=layout)
+    require_cuda()
+    vals = np.ascontiguousarray(vals)
+    packed = np.empty((vals.size * bits + 7) // 8, dtype=np.uint8)
+    scale, zero = C.c_double(), C.c_double()
+    _lib.call("pkv_quantize_group_host", vals.ctypes.data_as(C.c_void_p), vals.size, bits, C.byref(scale),
+              C.byref(zero), packed.ctypes.data_as(C.c_void_p))
+    return QuantizedGroup(params=QuantParams(scale=scale.value, zero_point=zero.value, bits=bits),
+                          codes=packed.tobytes(), length=vals.size, layout=layout)
 
 
 def dequantize_group(group: QuantizedGroup) -> np.ndarray:
-    """scale * code + zero_point in float64 (quant.py:114-117)."""
-    codes = torch.from_numpy(unpack_codes(group.codes, group.length, group.params.bits)).cuda().to(torch.float64)
-    out = codes * group.params.scale
-    out = out + group.params.zero_point
-    return out.cpu().numpy()
+    """scale * code + zero_point in float64 (quant.py:114-117), on the GPU."""
+    bits, n = group.params.bits, group.length
+    _check_bits(bits)
+    expected = (n * bits + 7) // 8
+    if len(group.codes) != expected:
+        raise DataError(f"packed payload is {len(group.codes)} bytes, expected {expected} for {n} codes of {bits} bits")
+    out = np.empty(n, dtype=np.float64)
+    if n:
+        require_cuda()
+        src = np.frombuffer(bytes(group.codes), dtype=np.uint8)
+        _lib.call("pkv_dequantize_group_host", src.ctypes.data_as(C.c_void_p), n, bits, C.c_double(group.params.scale),
+                  C.c_double(group.params.zero_point), out.ctypes.data_as(C.c_void_p))
+    return out
 
 
 def pack_codes(codes: np.ndarray, bits: int) -> bytes:

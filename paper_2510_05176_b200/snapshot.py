@@ -230,10 +230,23 @@ class SnapshotState:
     window_v: list = field(default_factory=list)
     v_decisions: list = field(default_factory=list)
     k_decisions: list = field(default_factory=list)
+    _facade: object = field(default=None, repr=False, compare=False)
 
     @property
     def gate(self) -> GateConfig:
         return GateConfig.create(self.head_dim, self.config.alpha)
+
+    def device_state(self):
+        """This state resumed on the GPU as an engine.HeadCacheState (one-unit cache via
+        pkv_cache_import), created once; the engine's functions route a loaded snapshot
+        state through it (reconstruct_token, committed_matrices, append_decode_token ...)."""
+        if self._facade is None:
+            import torch
+
+            from .engine import HeadCacheState
+            cache, _ = restore_cache({(0, 0): self}, dtype=torch.float64)
+            self._facade = HeadCacheState(self.config, self.head_dim, _cache=cache, _unit=0)
+        return self._facade
 
 
     @property
