@@ -532,6 +532,7 @@ __device__ __noinline__ void b_tile(const unsigned char* X, const float* M, Pat 
         inf = 1 | (chx << 1) | (chn << 8);
       }
     }
+    __syncwarp();  // every lane's reads of this token's kmx/kmn (stage D) precede the store
     if (q == 0) {
       const int t = t0 + 8 * h;
       sc.kmx()[t] = kx; sc.kmn()[t] = kn; sc.xmx()[t] = xx; sc.xmn()[t] = xn;
@@ -725,6 +726,7 @@ __device__ __noinline__ void token_stage(Scr sc, Pat pt, const unsigned char* X,
         b_tile<SIDE == 1>(X, M, pt, sc, tb, lane, idx[0], idx[1]);
       }
     }
+    __syncwarp();  // the tile's guess/cand reads precede their reuse as row offsets
     if (q == 0) {
       sc.fidx()[t0] = idx[0]; sc.fidx()[t0 + 8] = idx[1];
       if constexpr (SIDE == 0) {  // K: the final row's float offsets for even / odd channel chunks
@@ -959,6 +961,7 @@ __device__ __noinline__ void k_slow(const unsigned char* X, const float* M, Pat 
         dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
         dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
       }
+      __syncwarp();  // the group's info/kmx/kmn reads precede the exact-extrema store
       if (slow && g == 0) {
         sc.kmx()[ch] = __int_as_float(__double2hiint(dmx)); sc.xmx()[ch] = __int_as_float(__double2loint(dmx));
         sc.kmn()[ch] = __int_as_float(__double2hiint(dmn)); sc.xmn()[ch] = __int_as_float(__double2loint(dmn));

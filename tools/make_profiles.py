@@ -57,7 +57,8 @@ def main():
     units = int(os.environ.get("PROF_UNITS", 2 * 32 * 8)) * int(os.environ.get("PROF_COMMITTED", 32768 - 128))
     # only reports from this capture: within an hour of the newest one (older reports left in
     # gpurun_out/ by earlier captures would describe superseded kernels)
-    reps = {n: os.path.join(OUT, n + ".ncu-rep")
+    pre = os.environ.get("PROF_PREFIX", "")  # e.g. "r2_" for tools/gpu_r2.sh captures
+    reps = {n: os.path.join(OUT, pre + n + ".ncu-rep")
             for n in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn")}
     newest = max((os.path.getmtime(r) for r in reps.values() if os.path.exists(r)), default=0.0)
     for name, rep in reps.items():
@@ -72,7 +73,7 @@ def main():
         txt += "\n\nhot source lines (share of executed instructions / of stall samples):\n" + lines(rep)
         with open(os.path.join(PROF, f"{tag}_{name}.txt"), "w") as f:
             f.write(f"# ncu --set full capture: {name}.ncu-rep ({tag})\n\n" + txt)
-        if name.endswith("_full") and "dram__bytes_read.sum" in raw and "kmeans" not in name:
+        if "dram__bytes_read.sum" in raw and "kmeans" not in name:
             def to_bytes(v):
                 val, unit = float(v[0].replace(",", "")), v[1]
                 return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
@@ -87,7 +88,7 @@ def main():
                                  f"per token-unit of the captured launch ({units} token-units)",
                        "bytes_per_token_unit": traffic,
                        "warp_instr_per_token_unit": instr}, f, indent=1)
-    lp = os.path.join(OUT, "launches.csv")
+    lp = os.path.join(OUT, pre + "launches.csv")
     if os.path.exists(lp):
         with open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w") as f:
             f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 "
