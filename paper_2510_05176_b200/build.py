@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpkv_b200.so")
-SOURCES = ["pkv_encode.cu", "pkv_encode_tc.cu", "pkv_mine.cu", "pkv_attn.cu", "pkv_misc.cu", "pkv_capi.cu"]
+SOURCES = ["pkv_encode.cu", "pkv_encode_tc.cu", "pkv_mine.cu", "pkv_attn.cu", "pkv_attn_tc.cu", "pkv_misc.cu", "pkv_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -580,7 +580,9 @@ template <typename T>
 cudaError_t launch_attn(const DevCache& c, const AttnArgs& a, int Pk_max, int Pv_max, int win_len, int win_slot0,
                         float* out, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  if (a.nb > 0) {
+  if (a.nb > 0) e = launch_attn_tc(c, a, Pk_max, Pv_max, st);  // K3-TC (pkv_attn_tc.cu)
+  if (a.nb > 0 && e == cudaErrorNotSupported) {
+    e = cudaSuccess;
     const int nt = a.G <= 4 ? 1 : 2;
     size_t smem = attn_smem_bytes(c.Dp, Pk_max, Pv_max, c.bits, nt);
     if (smem > 227 * 1024) return cudaErrorNotSupported;  // pkv_decode_attn reports the pattern-count limit

@@ -868,6 +868,7 @@ static int attn_impl(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, 
   // enough CTAs for ~4 waves at 4 CTAs/SM, >= 4 blocks per chunk (one per warp)
   const int target = 16 * num_sms;
   int nchunk = std::max(1, std::min((target + c->U - 1) / c->U, (a.nb + 3) / 4));
+  nchunk = std::max(nchunk, (a.nb + 255) / 256);  // K3-TC: <= 256 blocks per chunk (s32 digit sums)
   a.bpc = std::max(1, (a.nb + nchunk - 1) / nchunk);
   a.nchunk = std::max(1, (a.nb + a.bpc - 1) / a.bpc);
   const size_t need = (size_t)c->U * a.nchunk * gqa * (c->Dp + 2) * 4;

@@ -283,6 +283,9 @@ cudaError_t launch_probes(const DevCache&, cudaStream_t);
 cudaError_t launch_import(const DevCache& c, int nb, int64_t C, const double* kparam, const int32_t* kidx,
                           const int32_t* vidx, const double* vparam, const uint8_t* kcodes, const uint8_t* vcodes,
                           const double* kdiag, const double* vdiag, cudaStream_t st);
+// K3-TC decode attention on tcgen05 kind::i8 (pkv_attn_tc.cu); cudaErrorNotSupported outside its
+// envelope (the caller then runs the CUDA-core K3)
+cudaError_t launch_attn_tc(const DevCache& c, const AttnArgs& a, int Pk_max, int Pv_max, cudaStream_t st);
 // K1-TC persistent fp16 prefill encoder (pkv_encode_tc.cu); cudaErrorNotSupported outside its envelope
 cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, const __half* v, int64_t rows,
                              int64_t unit_stride, int first_block, int nblocks, cudaStream_t st);

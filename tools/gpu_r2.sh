@@ -20,7 +20,7 @@ B="python bench.py --steps 2 --warmup 3 --no-four-bit --no-cpu --legs none"
 MED="python bench.py --batch 2 --layers 32 --tokens 32768 --pool 64 --steps 1 --warmup 3 --no-four-bit --no-cpu --e2e-pool 8 --legs none"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_launches_bench.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:encode_tc -s 2 -c 1 -o gpurun_out/${TAG}_prof_encode -f $MED > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_chunk -s 3 -c 1 -o gpurun_out/${TAG}_prof_attn -f $MED > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_tc -s 3 -c 1 -o gpurun_out/${TAG}_prof_attn -f $MED > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:kmeans -s 1 -c 1 -o gpurun_out/${TAG}_prof_kmeans -f python bench.py --batch 1 --layers 4 --tokens 32768 --pool 32 --steps 1 --warmup 3 --no-four-bit --no-cpu --e2e-pool 8 --legs none > /dev/null 2>&1
 fi
 if [ -z "$NO_SAN" ]; then
