@@ -782,7 +782,7 @@ def main():
                         "frac": r["att_gbps"] / peak, "bytes_per_step": r["att_bytes"], "gqa": args.gqa,
                         "context": T, "e2e_ms_per_step": e2e["attn_ms"],
                         "e2e_h2d_bytes": e2e["attn_h2d"], "e2e_d2h_bytes": e2e["attn_d2h"],
-                        "kernel": "attn_chunk_kernel + attn_merge_kernel", "clocks": r["clk_a"],
+                        "kernel": "attn_tc_kernel (K3-TC: tcgen05 kind::i8, integer code planes from TMEM) + attn_merge_kernel", "clocks": r["clk_a"],
                         "traffic": ncu_traffic("attn", U * committed)},
         "mining": {"ms": r["mine_ms"], "units": pool, "sides": 2, "tokens": T, "patterns": args.patterns,
                    "scratch": "preallocated outside the timed region (PatternKVCache.reserve_mining)",

@@ -12,7 +12,7 @@ C=paper_2510_05176_b200/csrc
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
   -I$C -Iinclude -c "$3" -o _ab/$1_var.o 2>&1 | grep -i "error" || true
 objs=""
-for s in pkv_encode pkv_encode_tc pkv_mine pkv_attn pkv_misc pkv_capi; do
+for s in pkv_encode pkv_encode_tc pkv_mine pkv_attn pkv_attn_tc pkv_misc pkv_capi; do
   if [ "$s" = "$2" ]; then objs="$objs _ab/$1_var.o"; else objs="$objs $B/$s.o"; fi
 done
 nvcc -shared -gencode arch=compute_100a,code=sm_100a $objs -o _ab/$1.so -lcudart
