@@ -226,6 +226,27 @@ __device__ __forceinline__ float zcode(float r, float lo32, float inv, float hg,
   bad |= fabsf(d) > hg;
   return z;
 }
+// two elements at once on the packed fp32 pipe (FADD2 / FFMA2: lane-wise the same IEEE RN
+// operations as zcode -- r - lo == r + (-lo), |d| > hg <=> |d| - hg > 0 without underflow to
+// zero); per-element params (K: two channels) with nhg = -hg
+__device__ __forceinline__ float2 zcode2(float2 r, float2 nlo, float2 inv, float2 nhg, bool& bad) {
+  const float2 rl = __fadd2_rn(r, nlo);
+  const float2 z = __ffma2_rn(rl, inv, make_float2(MAGIC, MAGIC));
+  const float2 k = __fadd2_rn(z, make_float2(-MAGIC, -MAGIC));
+  const float2 d = __ffma2_rn(rl, inv, make_float2(-k.x, -k.y));
+  const float2 e = __fadd2_rn(make_float2(fabsf(d.x), fabsf(d.y)), nhg);
+  bad |= fmaxf(e.x, e.y) > 0.f;  // fmaxf skips a NaN element (token past the span), as zcode's compare does
+  return z;
+}
+// shared params (V: one token)
+__device__ __forceinline__ float2 zcode2s(float2 r, float2 nlo, float2 inv, float hg, bool& bad) {
+  const float2 rl = __fadd2_rn(r, nlo);
+  const float2 z = __ffma2_rn(rl, inv, make_float2(MAGIC, MAGIC));
+  const float2 k = __fadd2_rn(z, make_float2(-MAGIC, -MAGIC));
+  const float2 d = __ffma2_rn(rl, inv, make_float2(-k.x, -k.y));
+  bad |= fmaxf(fabsf(d.x), fabsf(d.y)) > hg;
+  return z;
+}
 __device__ __forceinline__ uint32_t zpair(float z0, float z1) {
   return __byte_perm(__float_as_uint(z0), __float_as_uint(z1), 0x5410);
 }
@@ -383,8 +404,11 @@ __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* 
     const float4 m1 = *reinterpret_cast<const float4*>(m1p + 4 * (j ^ sw1));
     const float x0[4] = {h2f_lo(a0), h2f_hi(a0), h2f_lo(a2), h2f_hi(a2)};
     const float x1[4] = {h2f_lo(a1), h2f_hi(a1), h2f_lo(a3), h2f_hi(a3)};
-    const float rv[2][4] = {{__fsub_rn(x0[0], m0.x), __fsub_rn(x0[1], m0.y), __fsub_rn(x0[2], m0.z), __fsub_rn(x0[3], m0.w)},
-                            {__fsub_rn(x1[0], m1.x), __fsub_rn(x1[1], m1.y), __fsub_rn(x1[2], m1.z), __fsub_rn(x1[3], m1.w)}};
+    const float2 ra = __fadd2_rn(make_float2(x0[0], x0[1]), make_float2(-m0.x, -m0.y));
+    const float2 rb = __fadd2_rn(make_float2(x0[2], x0[3]), make_float2(-m0.z, -m0.w));
+    const float2 rc = __fadd2_rn(make_float2(x1[0], x1[1]), make_float2(-m1.x, -m1.y));
+    const float2 rd = __fadd2_rn(make_float2(x1[2], x1[3]), make_float2(-m1.z, -m1.w));
+    const float rv[2][4] = {{ra.x, ra.y, rb.x, rb.y}, {rc.x, rc.y, rd.x, rd.y}};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const float* xx = h ? x1 : x0;
@@ -424,8 +448,9 @@ __device__ __forceinline__ void resid_row(const unsigned char* X, const float* M
     ldsm_x2(xbase + (j >> 2) * 16384 + lrow * 128 + ((((2 * (j & 3) + lchk) ^ (lrow & 7))) << 4), a0, a1);
     const float4 m = *reinterpret_cast<const float4*>(mp + 4 * (j ^ sw));
     const float x[4] = {h2f_lo(a0), h2f_hi(a0), h2f_lo(a1), h2f_hi(a1)};
-    r[j][0] = __fsub_rn(x[0], m.x); r[j][1] = __fsub_rn(x[1], m.y);
-    r[j][2] = __fsub_rn(x[2], m.z); r[j][3] = __fsub_rn(x[3], m.w);
+    const float2 ra = __fadd2_rn(make_float2(x[0], x[1]), make_float2(-m.x, -m.y));
+    const float2 rb = __fadd2_rn(make_float2(x[2], x[3]), make_float2(-m.z, -m.w));
+    r[j][0] = ra.x; r[j][1] = ra.y; r[j][2] = rb.x; r[j][3] = rb.y;
     const float k0 = fkey(r[j][0], 4 * j + 0, 0xffffffe0u), k1 = fkey(r[j][1], 4 * j + 1, 0xffffffe0u);
     const float k2 = fkey(r[j][2], 4 * j + 2, 0xffffffe0u), k3 = fkey(r[j][3], 4 * j + 3, 0xffffffe0u);
     kmx = fmax3(kmx, k0, k1); kmx = fmax3(kmx, k2, k3);
@@ -760,8 +785,9 @@ __device__ __forceinline__ void k_load(const unsigned char* X, const float* M, c
     const uint32_t xb = *reinterpret_cast<const uint32_t*>(rowp + (((ck + 1) ^ (t & 7)) << 4));
     // mslot(p, q, jb) = q*32 + 4 ((jb ^ 2q) & 7) + (+-4 (p & 1), folded into fi[e])
     const float4 m = *reinterpret_cast<const float4*>(M + fi[e] + q * 32 + 4 * ((jb ^ (2 * q)) & 7));
-    rr[e][0] = __fsub_rn(h2f_lo(xa), m.x); rr[e][1] = __fsub_rn(h2f_hi(xa), m.y);
-    rr[e][2] = __fsub_rn(h2f_lo(xb), m.z); rr[e][3] = __fsub_rn(h2f_hi(xb), m.w);
+    const float2 ra = __fadd2_rn(make_float2(h2f_lo(xa), h2f_hi(xa)), make_float2(-m.x, -m.y));
+    const float2 rb = __fadd2_rn(make_float2(h2f_lo(xb), h2f_hi(xb)), make_float2(-m.z, -m.w));
+    rr[e][0] = ra.x; rr[e][1] = ra.y; rr[e][2] = rb.x; rr[e][3] = rb.y;
     if (!FULL && t >= L) rr[e][0] = rr[e][1] = rr[e][2] = rr[e][3] = FE_NAN;
   }
 }
@@ -871,15 +897,16 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
   const int slot0 = 2 * (jb % HS);
   const int wbase = 2 * (jb / HS);
   uint32_t badm = 0;
+  const float2 nlo01 = make_float2(-qlo[0], -qlo[1]), nlo23 = make_float2(-qlo[2], -qlo[3]);
+  const float2 inv01 = make_float2(qinv[0], qinv[1]), inv23 = make_float2(qinv[2], qinv[3]);
+  const float2 nhg01 = make_float2(-qhg[0], -qhg[1]), nhg23 = make_float2(-qhg[2], -qhg[3]);
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const int t = 16 * (e >> 1) + 8 * (e & 1) + g;
     bool bad0 = false, bad1 = false;
-    const float z0 = zcode(rr[e][0], qlo[0], qinv[0], qhg[0], bad0);
-    const float z1 = zcode(rr[e][1], qlo[1], qinv[1], qhg[1], bad0);
-    const float z2 = zcode(rr[e][2], qlo[2], qinv[2], qhg[2], bad1);
-    const float z3 = zcode(rr[e][3], qlo[3], qinv[3], qhg[3], bad1);
-    uint32_t p0 = zpair(z0, z1), p1 = zpair(z2, z3);
+    const float2 z01 = zcode2(make_float2(rr[e][0], rr[e][1]), nlo01, inv01, nhg01, bad0);
+    const float2 z23 = zcode2(make_float2(rr[e][2], rr[e][3]), nlo23, inv23, nhg23, bad1);
+    uint32_t p0 = zpair(z01.x, z01.y), p1 = zpair(z23.x, z23.y);
     if (!FULL && t >= L) { p0 = 0u; p1 = 0u; bad0 = bad1 = false; }
     badm |= ((uint32_t)bad0 << (2 * e)) | ((uint32_t)bad1 << (2 * e + 1));
     const uint32_t part = (p0 << (slot0 * BITS)) | (p1 << ((slot0 + 1) * BITS));
@@ -1069,13 +1096,14 @@ __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, in
   }
   uint32_t pp[16];
   uint32_t badm = 0;
+  const float2 nlo2 = make_float2(-lo32, -lo32), inv2 = make_float2(inv, inv);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     bool bad0 = false, bad1 = false;
-    const float z0 = zcode(r[j][0], lo32, inv, hg, bad0), z1 = zcode(r[j][1], lo32, inv, hg, bad0);
-    const float z2 = zcode(r[j][2], lo32, inv, hg, bad1), z3 = zcode(r[j][3], lo32, inv, hg, bad1);
-    pp[2 * j] = zpair(z0, z1);
-    pp[2 * j + 1] = zpair(z2, z3);
+    const float2 z01 = zcode2s(make_float2(r[j][0], r[j][1]), nlo2, inv2, hg, bad0);
+    const float2 z23 = zcode2s(make_float2(r[j][2], r[j][3]), nlo2, inv2, hg, bad1);
+    pp[2 * j] = zpair(z01.x, z01.y);
+    pp[2 * j + 1] = zpair(z23.x, z23.y);
     badm |= ((uint32_t)bad0 << (2 * j)) | ((uint32_t)bad1 << (2 * j + 1));
   }
   if (t >= L) {
