@@ -953,48 +953,51 @@ __device__ __noinline__ void k_fix(const double* kparam64, const Scr sc, int jb,
   }
 }
 // groups of chunk jb with several elements inside the fp32 error window: exact fp64 extrema
-// over the window (the 8 lanes of a channel cooperate), stored as double halves in
-// (kmx, xmx) / (kmn, xmn) with info = 1 << 16
+// over the window, stored as double halves in (kmx, xmx) / (kmn, xmn) with info = 1 << 16.
+// Only the slow channels are visited, each by the whole warp (lane = 4 tokens), so a chunk
+// with one slow channel costs 4 element steps per lane instead of 16 per channel quad.
 template <bool FULL>
 __device__ __noinline__ void k_slow(const unsigned char* X, const float* M, Pat pt, Scr sc, int jb, int lane, int L,
                                     const double* p64, unsigned* stats) {
   SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(pt.base); SMEM_PTR(sc.base);
   warp_converged();
-  const int g = lane >> 2, q = lane & 3;
+  uint32_t todo = __ballot_sync(0xffffffffu, lane < 16 && !(sc.info()[16 * jb + (lane & 15)] & 1)) & 0xffffu;
+  __syncwarp();  // every lane's info read precedes the stores below
 #pragma unroll 1
-  for (int kk = 0; kk < 4; ++kk) {
-    const int ch = 16 * jb + 2 * q + (kk & 1) + 8 * (kk >> 1);
-    const bool slow = !(sc.info()[ch] & 1);
-    if (__any_sync(0xffffffffu, slow)) {
-      const float gmx = sc.kmx()[ch], gmn = sc.kmn()[ch];
-      const float Rm = fmaxf(fabsf(gmx), fabsf(gmn));
-      const float tolx = TWO_M17 * Rm + 4.76837158203125e-07f * pt.mabsc()[ch];
-      const float hib = gmx - tolx, lob = gmn + tolx;
-      const int jj = ch >> 4, k4 = 2 * ((ch >> 3) & 1) + (ch & 1);
-      double dmx = -__longlong_as_double(0x7ff0000000000000LL), dmn = -dmx;
-#pragma unroll 1
-      for (int e = 0; e < 16; ++e) {
-        const int t = 16 * (e >> 1) + 8 * (e & 1) + g;
-        const int p = sc.fidx()[t];
-        const float xv = xt_at(X, t, ch);
-        const float key = fkey(__fsub_rn(xv, M[p * 128 + mslot(p, q, jj) + k4]), (uint32_t)e, 0xfffffff0u);
-        const bool in = (FULL || t < L) && (key >= hib || key <= lob);
-        const double v64 = in ? __dsub_rn((double)xv, p64[(int64_t)p * 128 + ch]) : 0.0;
-        if (in && key >= hib) dmx = fmax(dmx, v64);
-        if (in && key <= lob) dmn = fmin(dmn, v64);
-      }
+  while (todo) {
+    const int cc = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int ch = 16 * jb + cc;
+    const float gmx = sc.kmx()[ch], gmn = sc.kmn()[ch];
+    const float Rm = fmaxf(fabsf(gmx), fabsf(gmn));
+    const float tolx = TWO_M17 * Rm + 4.76837158203125e-07f * pt.mabsc()[ch];
+    const float hib = gmx - tolx, lob = gmn + tolx;
+    // the channel's slot in k_pass's layout: ch = 16 jb + 2q + {0,1,8,9}
+    const int q = (ch >> 1) & 3, k4 = 2 * ((ch >> 3) & 1) + (ch & 1);
+    double dmx = -__longlong_as_double(0x7ff0000000000000LL), dmn = -dmx;
 #pragma unroll
-      for (int o = 4; o <= 16; o <<= 1) {
-        dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
-        dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
-      }
-      __syncwarp();  // the group's info/kmx/kmn reads precede the exact-extrema store
-      if (slow && g == 0) {
-        sc.kmx()[ch] = __int_as_float(__double2hiint(dmx)); sc.xmx()[ch] = __int_as_float(__double2loint(dmx));
-        sc.kmn()[ch] = __int_as_float(__double2hiint(dmn)); sc.xmn()[ch] = __int_as_float(__double2loint(dmn));
-        sc.info()[ch] = 1 << 16;
-        if (stats) atomicAdd(&stats[3], 1u);
-      }
+    for (int i = 0; i < 4; ++i) {
+      const int t = lane + 32 * i;
+      const int e = 2 * (t >> 4) + ((t >> 3) & 1);  // k_pass element index of token t (key bits)
+      const int p = sc.fidx()[t];
+      const float xv = xt_at(X, t, ch);
+      const float key = fkey(__fsub_rn(xv, M[p * 128 + mslot(p, q, jb) + k4]), (uint32_t)e, 0xfffffff0u);
+      const bool in = (FULL || t < L) && (key >= hib || key <= lob);
+      const double v64 = in ? __dsub_rn((double)xv, p64[(int64_t)p * 128 + ch]) : 0.0;
+      if (in && key >= hib) dmx = fmax(dmx, v64);
+      if (in && key <= lob) dmn = fmin(dmn, v64);
+    }
+#pragma unroll
+    for (int o = 1; o <= 16; o <<= 1) {
+      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+    }
+    __syncwarp();  // every lane's kmx / kmn reads of this channel precede the store
+    if (lane == 0) {
+      sc.kmx()[ch] = __int_as_float(__double2hiint(dmx)); sc.xmx()[ch] = __int_as_float(__double2loint(dmx));
+      sc.kmn()[ch] = __int_as_float(__double2hiint(dmn)); sc.xmn()[ch] = __int_as_float(__double2loint(dmn));
+      sc.info()[ch] = 1 << 16;
+      if (stats) atomicAdd(&stats[3], 1u);
     }
   }
 }
