@@ -865,8 +865,9 @@ static int attn_impl(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, 
   AttnArgs a;
   a.q = q; a.G = gqa; a.scale_log2 = sm_scale * 1.4426950408889634f;
   a.blk0 = blk0; a.nb = blk1 - blk0; a.ml = ml;
-  // enough CTAs for ~4 waves at 4 CTAs/SM, >= 4 blocks per chunk (one per warp)
-  const int target = 16 * num_sms;
+  // enough CTAs for ~4 waves (K3-TC: 4 CTAs/SM at GQA <= 4, 2 CTAs of two head halves above),
+  // >= 4 blocks per chunk (one per warp)
+  const int target = (gqa <= 4 ? 16 : 8) * num_sms;
   int nchunk = std::max(1, std::min((target + c->U - 1) / c->U, (a.nb + 3) / 4));
   nchunk = std::max(nchunk, (a.nb + 255) / 256);  // K3-TC: <= 256 blocks per chunk (s32 digit sums)
   a.bpc = std::max(1, (a.nb + nchunk - 1) / nchunk);
