@@ -114,7 +114,10 @@ class PatternKVCache:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _lib.load().pkv_cache_destroy(h)
+            try:
+                _lib.load().pkv_cache_destroy(h)
+            except Exception:  # interpreter shutdown: the module globals may already be gone
+                pass
             self._h = None
 
     # ---- introspection --------------------------------------------------------

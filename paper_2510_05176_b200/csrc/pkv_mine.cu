@@ -647,9 +647,10 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
 // per channel), so a Lloyd round costs ONE pass instead of three:
 //   * labels of round r on tcgen05 (distance GEMM vs the centers split hi + lo, TMEM
 //     accumulator, fp64 re-decision of near ties) -- as in the v1 kernel;
-//   * the objective of round r-1, sum_t ||x_t - c_r[l_{r-1}(t)]||^2 (patterns.py:121:
-//     the new means against the previous labels), fp64 from the smem tile;
-//   * the centroid sums of round r by the channel warps from the same tile.
+//   * the centroid sums of round r by the channel warps from the same tile;
+//   * the objective (patterns.py:121: the new means against the labels that built them)
+//     needs no pass: sum_t ||x_t||^2 (first seeding pass) minus per-cluster terms of the
+//     exact sums, in double-double (sk_objective).
 // The sums are exact in fp64 whenever T * max|x| < 2^29: fp16 values are multiples of
 // 2^-24, so every partial sum of at most T of them is a multiple of 2^-24 below 2^53 *
 // 2^-24 and every fp64 addition is exact -- the result is independent of the order and
@@ -658,8 +659,9 @@ kmeans_kernel(DevCache c, MineArgs<T> a, const __grid_constant__ CUtensorMap tmK
 // an empty-cluster repair) the sums are recomputed in numpy's point order (v1 code).
 // Farthest-point seeding streams the same ring: fp64 distances to the newest seed from
 // the smem tile, running minima in HBM, block argmax (lowest index on ties).
-// A round's objective is known one pass late, so the stop rule (patterns.py:123) of
-// round r-1 is applied after pass r: the labels/sums pass r also produced are dropped.
+// The stop rule (patterns.py:123) is applied right after each round's means, as in the
+// reference; a round whose sums are not the exact ones (repair, huge values) takes one
+// objective pass (fp64 distances from the smem tile).
 // =================================================================================
 constexpr int SK_THREADS = 384;   // warp 0 TMA, 1 MMA, 2-3 idle, 4-7 rows, 8-11 channels
 constexpr int SK_NS = 4;          // smem ring stages (even: split seeding gives each consumer group its own stages)
@@ -789,6 +791,39 @@ __device__ __forceinline__ float sk_d2_f32(uint32_t tile_s, int row, uint32_t s3
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
 
+// ---- double-double arithmetic (error-free transforms) for the objective identity --------
+struct DD { double h, l; };
+__device__ __forceinline__ DD two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
+  return DD{s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ DD two_prod(double a, double b) {
+  const double p = __dmul_rn(a, b);
+  return DD{p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.h, b.h);
+  const double e = __dadd_rn(s.l, __dadd_rn(a.l, b.l));
+  const double h = __dadd_rn(s.h, e);
+  return DD{h, __dsub_rn(e, __dsub_rn(h, s.h))};
+}
+// sum_c x_c^2 of tile row `row` in double-double (every x_c^2 of an fp16 value is exact in
+// fp64, so the pair carries the row's squared norm to ~2^-104 relative)
+__device__ __forceinline__ void sk_x2_row(uint32_t tile_s, int row, DD& acc) {
+#pragma unroll 2
+  for (int q = 0; q < 16; ++q) {
+    const uint4 v = lds128(sk_chunk(tile_s, row, q));
+    const __half* h = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const double x = h2d(h[e]);
+      const DD t = two_sum(acc.h, __dmul_rn(x, x));
+      acc.h = t.h;
+      acc.l = __dadd_rn(acc.l, t.l);
+    }
+  }
+}
+
 struct SkCounters { uint32_t gt, gm, gl; };  // tiles streamed, MMA tiles, label hand-offs
 
 enum { SK_SEED = 1, SK_ASSIGN = 2, SK_OBJ = 4, SK_SUMS = 8, SK_FIRST = 16, SK_SPLIT = 32 };
@@ -820,18 +855,59 @@ __device__ __forceinline__ void sk_block_argmax(double v, long long i, const SkS
   __syncthreads();
 }
 
+// Double-double block sum (every thread contributes; all threads get the result)
+__device__ __forceinline__ DD sk_block_sum_dd(DD v, const SkSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const DD w{__shfl_xor_sync(0xffffffffu, v.h, o), __shfl_xor_sync(0xffffffffu, v.l, o)};
+    v = dd_add(v, w);
+  }
+  double* lo = reinterpret_cast<double*>(sm.redi);
+  if (lane == 0) { sm.redv[warp] = v.h; lo[warp] = v.l; }
+  __syncthreads();
+  DD r{0.0, 0.0};
+  for (int w = 0; w < SK_THREADS / 32; ++w) r = dd_add(r, DD{sm.redv[w], lo[w]});
+  __syncthreads();
+  return r;
+}
+// Objective of the labels the current centers were built from (patterns.py:121,
+// sum_t ||x_t - c_l(t)||^2) without a pass over the points:
+//   sum_t ||x_t - c_l(t)||^2 = sum_t ||x_t||^2 - sum_j sum_c (2 c_jc S_jc - n_j c_jc^2)
+// with S_jc the cluster sums, exact in fp64 on the streamed path (kernel header), X2 =
+// sum_t ||x_t||^2 from the first seeding pass and every product split exactly (two_prod),
+// all in double-double: the only roundings are ~2^-104 of the terms, so the value is the
+// exact objective to ~2^-102 X2 / obj relative before the final rounding (the reference's
+// own einsum + pairwise sum rounds at ~1e-15).  Valid only when S holds the exact sums.
+__device__ double sk_objective(const SkSmem& sm, int k, DD X2) {
+  DD acc{0.0, 0.0};
+  for (int i = threadIdx.x; i < k * 128; i += SK_THREADS) {
+    const int j = i >> 7, cc = i & 127;
+    const double cv = sm.cen[j * 129 + cc], S = sm.acc[i], n = (double)sm.cnt[j];
+    const DD p = two_prod(cv, S);                 // c S
+    const DD q = two_prod(cv, cv);                // c^2
+    const DD r = two_prod(n, q.h);                // n c^2 (hi part)
+    acc = dd_add(acc, DD{2.0 * p.h, 2.0 * p.l});  // x 2 is exact
+    acc = dd_add(acc, DD{-r.h, -__fma_rn(n, q.l, r.l)});
+  }
+  const DD T = sk_block_sum_dd(acc, sm);
+  const DD d = two_sum(X2.h, -T.h);
+  return __dadd_rn(d.h, __dadd_rn(d.l, __dsub_rn(X2.l, T.l)));
+}
+
 // Split seeding: the row warps take the even tiles and the channel warps the odd ones.
 // With an even stage count each group owns its stages, so no group ever skips a phase of
 // a stage's mbarrier (a skipped phase would make the parity test ambiguous).
 // Seeding update of one tile row: running minimum of the fp64 squared distances to the
 // chosen seeds (exact fp64 only where the newest seed can lower it), argmax tracking.
 __device__ __forceinline__ void sk_seed_row(const SkSmem& sm, uint32_t tile_s, int s, int row, int64_t t, int mode,
-                                            double* near_, double& bv, long long& bi_out, float& xmax) {
+                                            double* near_, double& bv, long long& bi_out, float& xmax, DD& x2) {
   const uint32_t seed_s = smem_u32(sm.seed);
   double nv;
   if (mode & SK_FIRST) {
     nv = sk_d2x4<true>(tile_s, row, seed_s, &xmax);
     near_[t] = nv;
+    sk_x2_row(tile_s, row, x2);
   } else {
     nv = sm.sNear[s * 128 + row];
     const float lb = sk_d2_f32(tile_s, row, smem_u32(sm.seed32)) * 0.9999847412109375f;  // (1 - 2^-16)
@@ -847,7 +923,7 @@ __device__ __forceinline__ void sk_seed_row(const SkSmem& sm, uint32_t tile_s, i
 // (SK_OBJ) and its running argmax of the seeding minima (SK_SEED via bv/bi) and |x|max.
 __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUtensorMap* map, int64_t row_base,
                         SkCounters& ctr, double* near_, const int* lab_old, int* lab_new, double& obj, double& bv,
-                        long long& bi_out, float& xmax) {
+                        long long& bi_out, float& xmax, DD& x2) {
   using namespace sm100;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = (int)((Tn + 127) / 128);
@@ -1019,7 +1095,7 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
         mbar_arrive(&tempty[acc]);
       }
       if (live) {
-        if (seedp) sk_seed_row(sm, tile_s, s, row, t, mode, near_, bv, bi_out, xmax);
+        if (seedp) sk_seed_row(sm, tile_s, s, row, t, mode, near_, bv, bi_out, xmax, x2);
         if (assign) {
           lab_new[t] = bi;
           atomicAdd(&sm.cnt[bi], 1);
@@ -1089,7 +1165,7 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
         if (m & 1) {
           mbar_wait_sleep(&full[s], ph);
           const int64_t t = (int64_t)m * 128 + c;
-          if (t < Tn) sk_seed_row(sm, smem_u32(sk_tile(sm, s, 0)), s, c, t, mode, near_, bv, bi_out, xmax);
+          if (t < Tn) sk_seed_row(sm, smem_u32(sk_tile(sm, s, 0)), s, c, t, mode, near_, bv, bi_out, xmax, x2);
           mbar_arrive_cnt(&empty[s], 2);
         }
         continue;
@@ -1146,7 +1222,6 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
   double* near_ = a.near_ + so;
   double* own = a.own + so;
   int* lab = a.lab + so;
-  int* lab2 = a.lab2 + so;
   double* hist = a.hist + ((int64_t)u * 2 + side) * 25;
   double* p64 = (side == 0 ? c.kpat64 : c.vpat64) + (int64_t)u * c.Pcap * 128;
   float* p32 = (side == 0 ? c.kpat32 : c.vpat32) + (int64_t)u * c.Pcap * c.Dp;
@@ -1200,6 +1275,7 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
   double objp = 0.0, bv = -1.0 / 0.0;
   long long bi = 0x7fffffffffffffffLL;
   float xmax = 0.f;
+  DD x2sum{0.0, 0.0};  // this thread's share of sum_t ||x_t||^2 (first seeding pass)
 
   // ---- seeding (patterns.py:134-142) with distinct-rows detection -------------------
   const int64_t first = a.first[side][u];
@@ -1211,7 +1287,8 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
   }
   __syncthreads();
   const int split = (a.side_mask & 4) ? 0 : SK_SPLIT;  // bit 2: debugging switch (one consumer group)
-  sk_pass(SK_SEED | SK_FIRST | split, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
+  sk_pass(SK_SEED | SK_FIRST | split, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax, x2sum);
+  const DD X2 = sk_block_sum_dd(x2sum, sm);
   double vmax;
   long long imax;
   sk_block_argmax(bv, bi, sm, vmax, imax);
@@ -1240,7 +1317,7 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
     __syncthreads();
     bv = -1.0 / 0.0;
     bi = 0x7fffffffffffffffLL;
-    sk_pass(SK_SEED | split, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax);
+    sk_pass(SK_SEED | split, Tn, k, sm, map, row_base, ctr, near_, nullptr, nullptr, objp, bv, bi, xmax, x2sum);
     sk_block_argmax(bv, bi, sm, vmax, imax);
   }
 
@@ -1284,23 +1361,11 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
       sm.cen[j * 129 + cc] = (double)__half2float(X[(int64_t)chosen[j] * 128 + cc]);
     }
     __syncthreads();
-    int* lcur = lab;   // labels of the newest assignment
-    int* lprev = lab2; // labels the current centers were built from
+    int* lcur = lab;  // labels of the newest assignment (the centers are built from them)
     double prev = 1.0 / 0.0;
-    for (int r = 0; r <= 25; ++r) {
-      const int mode = (r < 25 ? (SK_ASSIGN | (exact_sums ? SK_SUMS : 0)) : 0) | (r > 0 ? SK_OBJ : 0);
-      objp = 0.0;
-      sk_pass(mode, Tn, k, sm, map, row_base, ctr, nullptr, lprev, lcur, objp, bv, bi, xmax);
-      if (r > 0) {
-        const double obj = sk_block_sum(objp, sm);
-        if (tid == 0) hist[r - 1] = obj;
-        iters = r;
-        if (obj == 0.0 || (isfinite(prev) && prev - obj < 1e-6 * prev) || r == 25) {
-          fin = lprev;
-          break;
-        }
-        prev = obj;
-      }
+    for (int r = 0; r < 25; ++r) {  // KMEANS_MAX_ITERS rounds (patterns.py:107-124)
+      sk_pass(SK_ASSIGN | (exact_sums ? SK_SUMS : 0), Tn, k, sm, map, row_base, ctr, nullptr, nullptr, lcur, objp, bv,
+              bi, xmax, x2sum);
       // ---- empty-cluster repair of the new labels (patterns.py:112-118) -----------------
       if (tid == 0) {
         int ne = 0;
@@ -1350,8 +1415,23 @@ kmeans_stream_kernel(DevCache c, MineArgs<__half> a, const __grid_constant__ CUt
         sm.cen[j * 129 + cc] = __ddiv_rn(sm.acc[i], (double)sm.cnt[j]);
       }
       __syncthreads();
-      int* tl = lprev; lprev = lcur; lcur = tl;
+      // ---- objective and stop rule (patterns.py:121-124) ---------------------------------
+      // exact sums: the double-double identity, no pass; otherwise (repair, huge values) an
+      // objective pass over the points (fp64 distance to the assigned center)
+      double obj;
+      if (!seq) {
+        obj = sk_objective(sm, k, X2);
+      } else {
+        objp = 0.0;
+        sk_pass(SK_OBJ, Tn, k, sm, map, row_base, ctr, nullptr, lcur, nullptr, objp, bv, bi, xmax, x2sum);
+        obj = sk_block_sum(objp, sm);
+      }
+      if (tid == 0) hist[r] = obj;
+      iters = r + 1;
+      if (obj == 0.0 || (isfinite(prev) && prev - obj < 1e-6 * prev)) break;
+      prev = obj;
     }
+    fin = lcur;
     n = k;
   }
   // ---- write the pattern tables -------------------------------------------------------
