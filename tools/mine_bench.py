@@ -11,7 +11,7 @@ cfg = P.EngineConfig(bits=2, pattern_count=int(os.environ.get("P", "32")))
 c = P.PatternKVCache(cfg, U, 128, dtype=torch.float16, max_tokens=T + 256)
 c.reserve_mining(T)
 ev = lambda: torch.cuda.Event(enable_timing=True)
-for i in range(3):
+for i in range(int(os.environ.get("REPS", "3"))):
     c.reset(keep_patterns=False)
     torch.cuda.synchronize()
     a, b, d, e, f, g = ev(), ev(), ev(), ev(), ev(), ev()
