@@ -11,6 +11,8 @@ Mining runs once before the timed region (reported under `mining`).
 Further legs (each its own JSON object, device-timed with CUDA events, max over ranks):
   decode_attn   one decode-attention step over the cfg2 cache (GQA 4)
   decode_loop   cfg2: 256 decode steps of append-and-refresh + attention (2 flushes)
+  refgen        the headline encode on units from the reference generator (numpy, restated),
+                with the K1-TC rare-path counters next to the torch-family pool's
   cfg3          Qwen2.5-7B: 28 layers x 4 KV heads, 126,976-token prefill + decode steps,
                 2-bit, GQA 7, P 32 -> 64 over 4096 steps; KV heads shard over <= 4 ranks,
                 a sequence split (pkv_decode_attn_partial + one (o, m, l) exchange) beyond
@@ -44,7 +46,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
-ALL_LEGS = ("decode_loop", "cfg3", "cfg4", "cfg5_head")
+ALL_LEGS = ("decode_loop", "refgen", "cfg3", "cfg4", "cfg5_head")
 
 
 def hbm_peak():
@@ -338,6 +340,98 @@ def leg_encode(ctx, bits: int, k, v, pool_patterns, results, want_e2e: bool):
     torch.cuda.empty_cache()
     results[bits] = r
     return pk, pv
+
+
+def k1tc_counters(ctx, k, v, bits):
+    """K1-TC rare-path counters of one encode pass over (k, v) [n, T, 128] with tables mined on
+    the same units: fp64 re-matches, exact-division code fix-ups, pruning survivors, slow
+    exact-extrema groups (per committed token-unit / group)."""
+    torch, args = ctx.torch, ctx.args
+    from paper_2510_05176_b200 import PatternKVCache, _lib
+    from paper_2510_05176_b200.cache import _ptr, _stream
+    from paper_2510_05176_b200.config import EngineConfig
+    n, T = k.shape[0], k.shape[1]
+    cfg = EngineConfig(bits=bits, pattern_count=args.patterns)
+    m = PatternKVCache(cfg, n, 128, dtype=torch.float16, max_tokens=T + 256)
+    m.reserve_mining(T)
+    m.prefill(k, v)
+    c2 = PatternKVCache(cfg, n, 128, dtype=torch.float16, max_tokens=T + 256, stats=True)
+    c2.set_patterns(0, m.patterns(0)[:, : args.patterns])
+    c2.set_patterns(1, m.patterns(1)[:, : args.patterns])
+    del m
+    c2.commit_prefill(k, v)
+    buf = torch.zeros(4, dtype=torch.int32, device="cuda")
+    _lib.call("pkv_cache_read", c2._h, b"stats", 0, 16, _ptr(buf), _stream())
+    s = buf.cpu().tolist()
+    tu = n * (T - 128)
+    return {"refines_per_token_unit": s[0] / tu, "code_fixups_per_element": s[1] / (tu * 256),
+            "survivors_per_token_side": s[2] / (2 * tu), "slow_groups_per_group": s[3] / (2 * tu)}
+
+
+def leg_refgen(ctx, k, v):
+    """Headline encode on units from the reference generator itself (analysis.py:321-370, restated
+    in paper_2510_05176_b200.synthetic; SURVEY 8(d) models: K outlier channel 3 x 32, drift 1/T,
+    noise 0.05; V 32 clusters, spread 5, within 0.2, consistency 0.9, vocab 1024; per-unit seed
+    1_000_003 b + 1_009 l + h), a pool tiled over the cfg2 batch as in `value`, plus the K1-TC
+    rare-path counters of that pool next to those of the torch-family pool (the pruning rate
+    decides encode speed).  Overwrites k, v (the headline legs are done)."""
+    torch, args = ctx.torch, ctx.args
+    from paper_2510_05176_b200 import PatternKVCache
+    from paper_2510_05176_b200 import synthetic as S
+    from paper_2510_05176_b200.config import EngineConfig
+    U, T, D, G = k.shape[0], k.shape[1], 128, 128
+    pool = min(args.refgen_pool, U)
+    km = S.KeyModel(outlier_channels=(3,), outlier_multipliers=(32.0,), drift_rate=1.0 / T, noise_std=0.05)
+    vm = S.ValueModel(cluster_count=32, center_spread=5.0, within_std=0.2, consistency=0.9, vocab_size=1024)
+    kp = torch.empty((pool, T, D), dtype=torch.float16)
+    vp = torch.empty((pool, T, D), dtype=torch.float16)
+    for u in range(pool):
+        b, l, h = u // (args.layers * args.kv_heads), (u // args.kv_heads) % args.layers, u % args.kv_heads
+        st = S.generate_synthetic_stream(S.SyntheticStreamSpec(
+            layers=1, heads=1, head_dim=D, prefill_len=T, decode_len=0, k_model=km, v_model=vm,
+            seed=1_000_003 * b + 1_009 * l + h))
+        kp[u] = torch.from_numpy(st.prefill_k[0, 0]).to(torch.float16)
+        vp[u] = torch.from_numpy(st.prefill_v[0, 0]).to(torch.float16)
+    kd, vd = kp.cuda(), vp.cuda()
+    del kp, vp
+    bits = args.bits
+    stats_synth = k1tc_counters(ctx, k[:pool], v[:pool], bits)
+    stats_ref = k1tc_counters(ctx, kd, vd, bits)
+    for u0 in range(0, U, pool):
+        n = min(pool, U - u0)
+        k[u0:u0 + n].copy_(kd[:n])
+        v[u0:u0 + n].copy_(vd[:n])
+    del kd, vd
+    cfgE = EngineConfig(bits=bits, pattern_count=args.patterns)
+    mcache = PatternKVCache(cfgE, pool, D, dtype=torch.float16, max_tokens=T + 2 * G)
+    mcache.reserve_mining(T)
+    mcache.prefill(k[:pool], v[:pool])  # warm
+    mcache.reset(keep_patterns=False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    mcache.prefill(k[:pool], v[:pool])
+    e1.record()
+    torch.cuda.synchronize()
+    mine_ms = e0.elapsed_time(e1)
+    reps = (U + pool - 1) // pool
+    cache = PatternKVCache(cfgE, U, D, dtype=torch.float16, max_tokens=T + 2 * G)
+    cache.set_patterns(0, mcache.patterns(0)[:, : args.patterns].repeat(reps, 1, 1)[:U])
+    cache.set_patterns(1, mcache.patterns(1)[:, : args.patterns].repeat(reps, 1, 1)[:U])
+    del mcache
+
+    def step():
+        cache.reset(keep_patterns=True)
+        cache.commit_prefill(k, v)
+
+    ms, clk = ctx.time_steps(step, args.steps, args.warmup)
+    enc_bytes = U * (T - 128) * enc_bytes_per_token(bits)
+    gbps = enc_bytes / (ms * 1e-3) / 1e9
+    del cache
+    return {"encode_GBps": ctx.world * gbps, "frac": gbps / ctx.peak, "ms_per_step": ms, "bits": bits, "units": U,
+            "pool": pool, "mining_ms_pool": mine_ms, "clocks": clk,
+            "generator": "paper_2510_05176_b200.synthetic.generate_synthetic_stream (reference analysis.py:321-370)",
+            "k1tc_counters_refgen": stats_ref, "k1tc_counters_torch_family": stats_synth}
 
 
 def leg_decode_loop(ctx, cache, k, v, q, out, bits):
@@ -679,6 +773,7 @@ def main():
     ap.add_argument("--e2e-slices", type=int, default=8, help="unit slices the e2e step streams (H2D || encode)")
     ap.add_argument("--legs", default=",".join(ALL_LEGS), help="extra legs: " + ",".join(ALL_LEGS) + " or none")
     ap.add_argument("--decode-steps", type=int, default=256)
+    ap.add_argument("--refgen-pool", type=int, default=32, help="reference-generator units tiled by the refgen leg")
     ap.add_argument("--cfg3-prefill", type=int, default=126976)
     ap.add_argument("--cfg3-steps", type=int, default=4096)
     ap.add_argument("--cfg4-steps", type=int, default=512)
@@ -717,6 +812,12 @@ def main():
     pats = None
     for bits in ([args.bits] + ([] if args.no_four_bit else [4 if args.bits != 4 else 2])):
         pats = leg_encode(ctx, bits, k, v, pats, results, want_e2e=(bits == args.bits))
+    refgen = None
+    if "refgen" in args.legs:
+        try:
+            refgen = leg_refgen(ctx, k, v)
+        except Exception as ex:  # reported, not fatal
+            refgen = {"failed": f"{type(ex).__name__}: {ex}"[:300]}
     del k, v
     torch.cuda.empty_cache()
     extra = {}
@@ -786,7 +887,8 @@ def main():
                         "traffic": ncu_traffic("attn", U * committed)},
         "mining": {"ms": r["mine_ms"], "units": pool, "sides": 2, "tokens": T, "patterns": args.patterns,
                    "scratch": "preallocated outside the timed region (PatternKVCache.reserve_mining)",
-                   "kernel": "kmeans_kernel<__half, TC>: distance GEMM on tcgen05 (TMA + TMEM), fp64 means/objective"},
+                   "kernel": "kmeans_stream_kernel: one TMA stream per pass, distance GEMM on tcgen05 (TMEM), exact fp64 "
+                             "centroid sums, objective from the sums in double-double"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e["gbps"], "unit": "GB/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms"],
@@ -808,6 +910,8 @@ def main():
                                    "decode_ms": o["att_ms"], "mining_ms": o["mine_ms"]}
         if "decode_loop" in o:
             line[f"bits{other[0]}"]["decode_loop"] = o["decode_loop"]
+    if refgen is not None:
+        line["refgen"] = refgen
     line.update(extra)
     print(json.dumps(line), flush=True)
     if ctx.world > 1:

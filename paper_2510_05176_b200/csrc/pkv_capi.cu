@@ -583,36 +583,20 @@ extern "C" int pkv_mine(pkv_cache* c, int32_t side, const void* x, int64_t T, co
   return mine_impl(c, 1 << side, x, x, T, first_idx, first_idx, history, niter, labels, (cudaStream_t)stream);
 }
 
-// pattern tables with per-unit counts (device [U][P][D] fp64, host counts [U] <= P)
+// pattern tables with per-unit counts (device [U][P][D] fp64, host counts [U] <= P): installed by
+// a kernel on the stream (no host round trip of the table)
 static int load_patterns(pkv_cache* c, int side, const double* pat, int P, const int32_t* counts, cudaStream_t st) {
-  DevCache& d = c->dev;
-  double* p64 = side == 0 ? d.kpat64 : d.vpat64;
-  float* p32 = side == 0 ? d.kpat32 : d.vpat32;
-  std::vector<double> h((size_t)c->U * P * c->D);
-  if (P > 0) CU(cudaMemcpyAsync(h.data(), pat, h.size() * 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  std::vector<double> h64((size_t)c->U * d.Pcap * c->D, 0.0);
-  std::vector<float> h32((size_t)c->U * d.Pcap * d.Dp, 0.f);
-  std::vector<float> pm(c->U, 0.f);
-  std::vector<int> n(c->U, 0);
-  int bound = 0;
-  for (int u = 0; u < c->U; ++u) {
-    n[u] = counts ? counts[u] : P;
-    bound = std::max(bound, n[u]);
-    for (int p = 0; p < n[u]; ++p)
-      for (int ch = 0; ch < c->D; ++ch) {
-        const double v = h[((size_t)u * P + p) * c->D + ch];
-        h64[((size_t)u * d.Pcap + p) * c->D + ch] = v;
-        h32[((size_t)u * d.Pcap + p) * d.Dp + ch] = (float)v;
-        pm[u] = std::max(pm[u], (float)std::fabs(v) * (1.f + 1e-6f));
-      }
+  int bound = P;
+  int* dcounts = nullptr;
+  if (counts) {
+    bound = 0;
+    for (int u = 0; u < c->U; ++u) bound = std::max(bound, (int)counts[u]);
+    CU(cudaMallocAsync((void**)&dcounts, (size_t)c->U * 4, st));
+    CU(cudaMemcpyAsync(dcounts, counts, (size_t)c->U * 4, cudaMemcpyHostToDevice, st));
   }
-  CU(cudaMemcpyAsync(p64, h64.data(), h64.size() * 8, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(p32, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(side == 0 ? d.kpmax : d.vpmax, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(side == 0 ? d.nk : d.nv, n.data(), n.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(launch_probes(d, st));
-  CU(cudaStreamSynchronize(st));
+  CU(launch_install_patterns(c->dev, side, pat, P, dcounts, st));
+  CU(launch_probes(c->dev, st));
+  if (dcounts) CU(cudaFreeAsync(dcounts, st));
   if (side == 0) c->pk_bound = bound; else c->pv_bound = bound;
   return PKV_OK;
 }
@@ -684,32 +668,7 @@ extern "C" int pkv_set_patterns(pkv_cache* c, int32_t side, const double* pat, i
   cudaStream_t st = (cudaStream_t)stream;
   int rc = reserve(c, c->dev.Tcap, std::max(c->dev.Pcap, P + 8), st);
   if (rc) return rc;
-  DevCache& d = c->dev;
-  double* p64 = side == 0 ? d.kpat64 : d.vpat64;
-  float* p32 = side == 0 ? d.kpat32 : d.vpat32;
-  std::vector<double> h((size_t)c->U * P * c->D);
-  if (P > 0) CU(cudaMemcpyAsync(h.data(), pat, h.size() * 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  std::vector<double> h64((size_t)c->U * d.Pcap * c->D, 0.0);
-  std::vector<float> h32((size_t)c->U * d.Pcap * d.Dp, 0.f);
-  std::vector<float> pm(c->U, 0.f);
-  std::vector<int> n(c->U, P);
-  for (int u = 0; u < c->U; ++u)
-    for (int p = 0; p < P; ++p)
-      for (int ch = 0; ch < c->D; ++ch) {
-        const double v = h[((size_t)u * P + p) * c->D + ch];
-        h64[((size_t)u * d.Pcap + p) * c->D + ch] = v;
-        h32[((size_t)u * d.Pcap + p) * d.Dp + ch] = (float)v;
-        pm[u] = std::max(pm[u], (float)std::fabs(v) * (1.f + 1e-6f));
-      }
-  CU(cudaMemcpyAsync(p64, h64.data(), h64.size() * 8, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(p32, h32.data(), h32.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(side == 0 ? d.kpmax : d.vpmax, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(side == 0 ? d.nk : d.nv, n.data(), n.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(launch_probes(d, st));
-  CU(cudaStreamSynchronize(st));
-  if (side == 0) c->pk_bound = P; else c->pv_bound = P;
-  return PKV_OK;
+  return load_patterns(c, side, pat, P, nullptr, st);
 }
 
 // ---------------------------------------------------------------------------------

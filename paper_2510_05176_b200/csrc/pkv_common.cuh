@@ -280,6 +280,7 @@ cudaError_t launch_match(const double*, int64_t, const double*, int, int, int64_
 cudaError_t launch_midrange(const double*, int64_t, int, double*, cudaStream_t);
 size_t mine_smem_bytes(int k, int D, bool tc);
 cudaError_t launch_probes(const DevCache&, cudaStream_t);
+cudaError_t launch_install_patterns(const DevCache&, int, const double*, int, const int*, cudaStream_t);
 cudaError_t launch_import(const DevCache& c, int nb, int64_t C, const double* kparam, const int32_t* kidx,
                           const int32_t* vidx, const double* vparam, const uint8_t* kcodes, const uint8_t* vcodes,
                           const double* kdiag, const double* vdiag, cudaStream_t st);

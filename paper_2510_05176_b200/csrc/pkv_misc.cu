@@ -142,6 +142,40 @@ cudaError_t launch_probes(const DevCache& c, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---- pattern-table install (pkv_set_patterns / snapshot import): device [U][P][D] fp64
+// -> the fp64 / fp32 arenas (rows past a unit's count zeroed), per-unit count and
+// max |m| (x (1 + 1e-6), the bound the matchers use); no host round trip.
+__global__ void install_patterns_kernel(DevCache c, int side, const double* pat, int P, const int* counts) {
+  const int u = blockIdx.x;
+  const int n = counts ? counts[u] : P;
+  double* p64 = (side == 0 ? c.kpat64 : c.vpat64) + (int64_t)u * c.Pcap * c.D;
+  float* p32 = (side == 0 ? c.kpat32 : c.vpat32) + (int64_t)u * c.Pcap * c.Dp;
+  float m = 0.f;
+  for (int64_t i = threadIdx.x; i < (int64_t)c.Pcap * c.Dp; i += blockDim.x) {
+    const int p = (int)(i / c.Dp), ch = (int)(i % c.Dp);
+    const bool in = p < n && ch < c.D;
+    const double v = in ? pat[((int64_t)u * P + p) * c.D + ch] : 0.0;
+    if (ch < c.D) p64[(int64_t)p * c.D + ch] = v;
+    p32[i] = (float)v;
+    if (in) m = fmaxf(m, fabsf((float)v) * (1.f + 1e-6f));
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    (side == 0 ? c.kpmax : c.vpmax)[u] = m;
+    (side == 0 ? c.nk : c.nv)[u] = n;
+  }
+}
+cudaError_t launch_install_patterns(const DevCache& c, int side, const double* pat, int P, const int* counts,
+                                    cudaStream_t st) {
+  install_patterns_kernel<<<c.U, 256, 0, st>>>(c, side, pat, P, counts);
+  return cudaGetLastError();
+}
+
 // ---- fragment-layout addressing (inverse of frag_rc) -------------------------------
 struct CodeLoc { int word; int shift; };
 __device__ __forceinline__ CodeLoc frag_locate(int side, int row, int col16, int j, int bits, int WL) {
