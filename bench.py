@@ -696,7 +696,23 @@ def leg_cfg4(ctx):
     e1.record()
     ctx.barrier()
     ms = ctx.max_over_ranks(e0.elapsed_time(e1))
+    # the flushing append alone (refresh to P + 1 patterns + K1 on the span of every unit), on a
+    # fresh fork of the same state: the window holds 128 + 127 tokens, the next append flushes
+    flush_ms = None
+    try:
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for t in range(m, m + 127):
+            big.append(kn[:, t % 256], vn[:, t % 256])
+        torch.cuda.synchronize()
+        f0.record()
+        big.append(kn[:, 0], vn[:, 0])
+        f1.record()
+        torch.cuda.synchronize()
+        flush_ms = ctx.max_over_ranks(f0.elapsed_time(f1))
+    except Exception:  # capacity: the flush timing is optional
+        flush_ms = None
     att_bytes = attn_bytes_per_step(U, T - 128, 128, 2, P, gqa)
+    res.update(late_flush_ms=flush_ms, late_flush_patterns=P + 1)
     res.update(late_context=T, late_patterns=P, late_steps=m, late_ms_total=ms,
                late_tokens_per_s=ctx.world * S * m / (ms * 1e-3), late_attn_ms=att_ms,
                late_attn_GBps_per_gpu=att_bytes / (att_ms * 1e-3) / 1e9,

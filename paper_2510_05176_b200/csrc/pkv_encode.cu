@@ -21,6 +21,7 @@ constexpr int ENC_THREADS = 256;
 constexpr int NPROBE = 16;      // channels of the d_mm lower bound
 constexpr int PRUNE_PMAX = 64;  // pruned matcher serves tables of <= 64 patterns
 constexpr int PRUNE_MAXCAND = 6;
+constexpr int PRUNE_WIDE_PMAX = 256;  // match_pruned_wide: probe table in the pattern staging rows
 constexpr int MS_ROWS = 33;     // 32 staged patterns + one zero row (RAW payload)
 constexpr float TWO_M22 = 2.384185791015625e-07f;  // 2^-22
 constexpr float TWO_M21 = 4.76837158203125e-07f;   // 2^-21
@@ -507,6 +508,150 @@ __device__ void match_pruned(const DevCache& c, const EncSmem& sm, const SpanSrc
   }
 }
 
+// The same pruned search for 64 < P <= 32 NC (NC = 4 or 8: decode flushes after many
+// refreshes, e.g. cfg4's 156 patterns).  The probe table [NPROBE][32 NC] lives in the pattern
+// staging rows of sm.ms (16 KB at NC = 8, rows 0..31; the zero row 32 is untouched), so full
+// distances read pattern rows from the fp32 table in L2.  Lane l holds patterns l + 32 pc.
+__device__ __forceinline__ float coop_dmm_g(const EncSmem& sm, int t, int p, const float* p32, int Dp) {
+  const int lane = threadIdx.x & 31;
+  const int cc = 4 * lane;
+  float mx = -INF32, mn = INF32;
+  if (cc < sm.Dm) {
+    const float4 x4 = *reinterpret_cast<const float4*>(sm.xs + t * sm.DS + cc);
+    const float4 m4 = __ldg(reinterpret_cast<const float4*>(p32 + (int64_t)p * Dp + cc));
+    const float r0 = x4.x - m4.x, r1 = x4.y - m4.y, r2 = x4.z - m4.z, r3 = x4.w - m4.w;
+    mx = fmax3(fmaxf(r0, r1), r2, r3);
+    mn = fmin3(fminf(r0, r1), r2, r3);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  return mx - mn;
+}
+template <typename T, int NC>
+__device__ void match_pruned_wide(const DevCache& c, const EncSmem& sm, const SpanSrc<T>& src, int u, int64_t off,
+                                  int L, int P, const float* p32, const double* p64, float pmax) {
+  constexpr int PM = 32 * NC;
+  constexpr int TG = 2;  // tokens per probe-table pass (register budget of the inlined search)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int D = c.D, Dp = c.Dp;
+  float* mpk = sm.ms;  // [NPROBE][PM]
+  __syncthreads();     // every reader of the staged chunk-0 rows is done
+  for (int i = tid; i < NPROBE * PM; i += ENC_THREADS) {
+    const int k = i / PM, p = i - k * PM;
+    mpk[i] = p < P ? p32[(int64_t)p * Dp + sm.probe[k]] : 0.f;
+  }
+  __syncthreads();
+  for (int t0 = 16 * warp; t0 < 16 * warp + 16 && t0 < L; t0 += TG) {
+    float lb[TG][NC];
+#pragma unroll
+    for (int pc = 0; pc < NC; ++pc) {
+      float m[NPROBE];
+#pragma unroll
+      for (int k = 0; k < NPROBE; ++k) m[k] = mpk[k * PM + 32 * pc + lane];
+      const bool valid = 32 * pc + lane < P;
+#pragma unroll
+      for (int j = 0; j < TG; ++j) {
+        float a = -INF32, b = INF32;
+        const float4* xq = reinterpret_cast<const float4*>(sm.xp + (t0 + j) * NPROBE);
+#pragma unroll
+        for (int k4 = 0; k4 < NPROBE / 4; ++k4) {
+          const float4 x4 = xq[k4];
+          const float r0 = x4.x - m[4 * k4], r1 = x4.y - m[4 * k4 + 1];
+          const float r2 = x4.z - m[4 * k4 + 2], r3 = x4.w - m[4 * k4 + 3];
+          a = fmax3(a, r0, r1); a = fmax3(a, r2, r3);
+          b = fmin3(b, r0, r1); b = fmin3(b, r2, r3);
+        }
+        lb[j][pc] = valid ? a - b : INF32;
+      }
+    }
+#pragma unroll 1
+    for (int j = 0; j < TG; ++j) {
+      const int t = t0 + j;
+      if (t >= L) break;
+      float lbj[NC];  // token j's bounds by selects (a dynamic index would put lb in local memory)
+#pragma unroll
+      for (int pc = 0; pc < NC; ++pc)
+        lbj[pc] = j == 0 ? lb[0][pc] : (j == 1 ? lb[1][pc] : (j == 2 ? lb[TG > 2 ? 2 : 0][pc] : lb[TG > 3 ? 3 : 0][pc]));
+      // guess = lowest LB, lowest pattern index on ties
+      float gv = lbj[0];
+#pragma unroll
+      for (int pc = 1; pc < NC; ++pc) gv = fminf(gv, lbj[pc]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) gv = fminf(gv, __shfl_xor_sync(0xffffffffu, gv, o));
+      int gi = -1;
+#pragma unroll
+      for (int pc = 0; pc < NC; ++pc) {
+        const unsigned e = __ballot_sync(0xffffffffu, lbj[pc] == gv);
+        if (gi < 0 && e) gi = 32 * pc + __ffs(e) - 1;
+      }
+      const float tol2 = 2.f * TWO_M20 * (sm.xabs[t] + pmax);
+      float best = coop_dmm_g(sm, t, gi, p32, Dp);
+      int bi = gi;
+      float second = INF32;
+      const float bound = best + tol2;
+      unsigned cm[NC];
+      int ncand = 0;
+#pragma unroll
+      for (int pc = 0; pc < NC; ++pc) {
+        cm[pc] = __ballot_sync(0xffffffffu, lbj[pc] <= bound);
+        if ((gi >> 5) == pc) cm[pc] &= ~(1u << (gi & 31));
+        ncand += __popc(cm[pc]);
+      }
+      if (ncand > PRUNE_MAXCAND) {
+        // poorly separated token: exhaustive search (lane = pattern, rows from L2)
+        float w1 = INF32, w2 = INF32;
+        int wi = 0x7fffffff;
+        const float* xr = sm.xs + t * sm.DS;
+#pragma unroll 1
+        for (int pc = 0; pc < NC; ++pc) {
+          const int pp = 32 * pc + lane;
+          float mx = -INF32, mn = INF32;
+          if (pp < P) {
+            const float* mrow = p32 + (int64_t)pp * Dp;
+            for (int cc = 0; cc < sm.Dm; cc += 4) {
+              const float4 x4 = *reinterpret_cast<const float4*>(xr + cc);
+              const float4 q = __ldg(reinterpret_cast<const float4*>(mrow + cc));
+              const float r0 = x4.x - q.x, r1 = x4.y - q.y, r2 = x4.z - q.z, r3 = x4.w - q.w;
+              mx = fmax3(mx, r0, r1); mx = fmax3(mx, r2, r3);
+              mn = fmin3(mn, r0, r1); mn = fmin3(mn, r2, r3);
+            }
+          }
+          const float v = pp < P ? mx - mn : INF32;
+          top2_merge(w1, wi, w2, v, pp, INF32);  // lanes visit their patterns in increasing index
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ob1 = __shfl_xor_sync(0xffffffffu, w1, o);
+          const int obi = __shfl_xor_sync(0xffffffffu, wi, o);
+          const float ob2 = __shfl_xor_sync(0xffffffffu, w2, o);
+          top2_merge(w1, wi, w2, ob1, obi, ob2);
+        }
+        best = w1; bi = wi; second = w2;
+      } else {
+#pragma unroll 1
+        for (int pc = 0; pc < NC; ++pc) {
+          while (cm[pc]) {
+            const int p = 32 * pc + __ffs(cm[pc]) - 1;
+            cm[pc] &= cm[pc] - 1;
+            const float d = coop_dmm_g(sm, t, p, p32, Dp);
+            if (d < best || (d == best && p < bi)) { second = best; best = d; bi = p; }
+            else second = fminf(second, d);
+          }
+        }
+      }
+      int idx = bi;
+      if (second <= best + tol2) {
+        idx = refine_match64<T>(sm, span_row(src, u, off, t, D), t, p64, P, D, lane);
+        if (lane == 0 && c.stats) atomicAdd(&c.stats[0], 1u);
+      }
+      if (lane == 0) sm.fidx[t] = idx;
+    }
+  }
+}
+
 // Exhaustive fp32 matching (lane = pattern, chunks of 32) for any table size.
 template <typename T>
 __device__ void match_brute(const DevCache& c, const EncSmem& sm, const SpanSrc<T>& src, int u, int64_t off, int L,
@@ -618,7 +763,9 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
     const float* p32 = (side == 0 ? c.kpat32 : c.vpat32) + (int64_t)u * c.Pcap * Dp;
     const double* p64 = (side == 0 ? c.kpat64 : c.vpat64) + (int64_t)u * c.Pcap * D;
     const float pmax = P > 0 ? (side == 0 ? c.kpmax[u] : c.vpmax[u]) : 0.f;
-    const bool pruned = P > 0 && exact_in_f32<T>::value && P <= PRUNE_PMAX && c.prune;
+    // wide tables: the probe table must fit the 32 staging rows (head_dim >= 124 at 256 patterns)
+    const bool pruned = P > 0 && exact_in_f32<T>::value && c.prune &&
+                        (P <= PRUNE_PMAX || (P <= PRUNE_WIDE_PMAX && NPROBE * (P > 128 ? 256 : 128) <= 32 * sm.DS));
 
     __syncthreads();  // previous side done with smem
     if (tid < NPROBE) sm.probe[tid] = c.probe[((int64_t)u * 2 + side) * 16 + tid];
@@ -719,7 +866,9 @@ encode_span_kernel(DevCache c, SpanSrc<T> srck, SpanSrc<T> srcv, int first_block
 
     // ---- B. nearest pattern -------------------------------------------------------
     if (pruned) {
-      if (P > 32) match_pruned<T, true>(c, sm, src, u, off, L, P, p32, p64, pmax);
+      if (P > 128) match_pruned_wide<T, 8>(c, sm, src, u, off, L, P, p32, p64, pmax);
+      else if (P > PRUNE_PMAX) match_pruned_wide<T, 4>(c, sm, src, u, off, L, P, p32, p64, pmax);
+      else if (P > 32) match_pruned<T, true>(c, sm, src, u, off, L, P, p32, p64, pmax);
       else match_pruned<T, false>(c, sm, src, u, off, L, P, p32, p64, pmax);
     } else if (P > 0) {
       match_brute<T>(c, sm, src, u, off, L, P, p32, p64, pmax);

@@ -275,3 +275,33 @@ def test_long_decode_pattern_growth_vs_oracle(pkv):
     out = cache.decode_attention(torch.from_numpy(q).cuda()).cpu().numpy()
     ref = O.head_attention(h, q[0].astype(np.float64), 1.0 / math.sqrt(d))
     assert np.abs(out[0] - ref).max() / np.abs(ref).max() <= 1e-3
+
+
+def test_decode_flush_wide_pruned_matcher_vs_oracle(pkv):
+    """Decode flushes past 128 patterns per side on the pruned matcher for wide tables
+    (match_pruned_wide: 4 and then 8 pattern chunks per lane, probe table in the staging
+    rows): 8 + 125 patterns per side at head_dim 128, codes/indices bit-exact vs the oracle."""
+    from paper_2510_05176_b200.config import EngineConfig
+    from paper_2510_05176_b200.export import export_unit
+
+    d, tp, G = 128, 64, 16
+    steps = 125 * G + 5
+    k, v = O.synth_unit(O.unit_seed(6, 1, 3), tp + steps, d)
+    k = k.astype(np.float16).astype(np.float64)
+    v = v.astype(np.float16).astype(np.float64)
+    cfg = dict(bits=4, pattern_count=8, group_size=G, residual_window=G)
+    cache = pkv.PatternKVCache(EngineConfig(**cfg), 1, d, dtype=torch.float16, max_tokens=tp + steps + 64)
+    kt = torch.from_numpy(k).half().cuda()
+    vt = torch.from_numpy(v).half().cuda()
+    cache.prefill(kt[None, :tp], vt[None, :tp])
+    for t in range(tp, tp + steps):
+        cache.append(kt[None, t], vt[None, t])
+    h = O.replay(k[:tp], v[:tp], k[tp:], v[tp:], O.Knobs(**cfg))
+    st = export_unit(cache, 0, with_bytes=False)
+    assert len(st.kpat) == len(h.kpat) == 8 + 125
+    np.testing.assert_array_equal(st.kpat, h.kpat)
+    np.testing.assert_array_equal(st.vpat, h.vpat)
+    np.testing.assert_array_equal(st.k_idx, np.concatenate([b[5] for b in h.k_blocks]))
+    np.testing.assert_array_equal(st.k_codes, np.concatenate([b[4] for b in h.k_blocks]))
+    np.testing.assert_array_equal(st.v_idx, np.array([x[3] for x in h.v_tok]))
+    np.testing.assert_array_equal(st.v_codes, np.stack([x[2] for x in h.v_tok]))
