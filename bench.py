@@ -226,12 +226,18 @@ class Ctx:
         self.torch, self.dist, self.args = torch, dist, args
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # PKV_BENCH_BACKEND=gloo lets N ranks share fewer GPUs (a one-GPU rehearsal of the
+        # multi-rank path: collectives staged through host memory); the driver's runs use NCCL
+        self.backend = os.environ.get("PKV_BENCH_BACKEND", "nccl")
+        self.local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(self.local)
         if self.world > 1:
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
         self.peak, self.peak_kind = hbm_peak()
 
     def barrier(self):
@@ -242,7 +248,7 @@ class Ctx:
     def max_over_ranks(self, x: float) -> float:
         if self.world == 1:
             return x
-        t = self.torch.tensor([x], device="cuda", dtype=self.torch.float64)
+        t = self.torch.tensor([x], device="cuda" if self.backend == "nccl" else "cpu", dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -765,7 +771,7 @@ def leg_cfg5_head(ctx):
             "tokens_per_s": B / (ms * 1e-3), "tokens_per_s_80_layers": B / (ms * 1e-3) * L / 80,
             "attn_GBps_per_gpu": att_bytes / (att_ms * 1e-3) / 1e9,
             "attn_frac": att_bytes / (att_ms * 1e-3) / 1e9 / ctx.peak, "scaling": "strong",
-            "collective": "NCCL all_gather_into_tensor of [B, L, 8/N, 8, 128] fp32 per step" if ctx.world > 1
+            "collective": f"{ctx.backend.upper()} all_gather_into_tensor of [B, L, 8/N, 8, 128] fp32 per step" if ctx.world > 1
             else "none at N=1", "clocks": clk}
 
 
