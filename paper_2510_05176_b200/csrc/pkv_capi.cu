@@ -349,7 +349,7 @@ extern "C" int pkv_cache_destroy(pkv_cache* c) {
   DevCache& d = c->dev;
   void* ptrs[] = {d.kpat64, d.vpat64, d.kpat32, d.vpat32, d.kpmax, d.vpmax, d.nk, d.nv, d.probe, d.blk_start, d.blk_len,
                   d.kcodes, d.kparam32, d.kparam64, d.kidx, d.vcodes, d.vparam32, d.vparam64, d.vidx, d.kdiag,
-                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag, d.work, c->mine_scratch};
+                  d.vdiag, d.wk, d.wv, c->stats, c->part, c->scratch_flag, d.work, c->mine_scratch, d.fix};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (d.bad) cudaFree(d.bad);
@@ -712,9 +712,19 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
     SpanSrc<T_> sk{(const T_*)k, T * c->D, 0, INT64_MAX / 4};
     SpanSrc<T_> sv{(const T_*)v, T * c->D, 0, INT64_MAX / 4};
     cudaError_t e1 = cudaErrorNotSupported;
-    if constexpr (std::is_same<T_, __half>::value)
+    if constexpr (std::is_same<T_, __half>::value) {
+      // deferred K code fix-up list: ~1e-3 of the elements at cfg2; an overflow is fixed in line
+      const int64_t want = std::min<int64_t>(std::max<int64_t>((int64_t)c->U * c->nb * 16, 1 << 16), 1 << 26);
+      if (c->dev.fixcap < want) {
+        if (c->dev.fix) cudaFree(c->dev.fix);
+        c->dev.fix = nullptr;
+        c->dev.fixcap = 0;
+        if (cudaMalloc((void**)&c->dev.fix, (size_t)want * 8) == cudaSuccess) c->dev.fixcap = (int)want;
+        else (void)cudaGetLastError();
+      }
       e1 = launch_encode_tc(c->dev, std::max(c->pk_bound, c->pv_bound), (const __half*)k, (const __half*)v, T,
                             T * c->D, 0, c->nb, st);
+    }
     if (e1 == cudaErrorNotSupported) {
       (void)cudaGetLastError();
       e1 = launch_encode<T_>(c->dev, sk, sv, 0, c->nb, st);

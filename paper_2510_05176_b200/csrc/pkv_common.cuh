@@ -208,7 +208,10 @@ struct DevCache {
   void* wk; void* wv;
   // stats
   unsigned* stats;                // [0] fp64 refines, [1] exact-division fallbacks
-  int* work;                      // [4] work-queue counters of the K1-TC encoder (reset per launch)
+  int* work;                      // [4] work-queue counters of the K1-TC encoder (reset per launch);
+                                  // work[2] counts deferred K code fix-ups
+  unsigned long long* fix;        // [fixcap] deferred K code fix-ups of K1-TC (see kfix_kernel)
+  int fixcap;
   unsigned long long* bad;        // smallest nf_key of a non-finite input seen since the last prefill
 };
 

@@ -919,14 +919,20 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
   }
   return badm;
 }
-// exact fix-up of chunk jb's guard-band pairs (bits of badm) from the stored fp64 params
+// guard-band pairs of chunk jb (bits of badm): deferred to kfix_kernel through the cache's fix
+// list (word and shift of the pair in the block's global code words + its position), so the
+// fp64 reference sequence with its L2 reads of x, the pattern value and the params runs after
+// the encoder instead of on an item's critical path (a K item's fix-ups and the barrier waiting
+// for the warp with the most were ~1/4 of its time); in line (exact, from the stored fp64
+// params) only when the list is full.
 template <int BITS>
 __device__ __noinline__ void k_fix(const double* kparam64, const Scr sc, int jb, int lane, uint32_t badm,
                                    const __half* xsrc, const double* p64, int64_t blk, uint32_t* KW, uint32_t* wreg,
-                                   unsigned* stats) {
+                                   unsigned* stats, unsigned long long* fix, int fixcap, int* fixcnt) {
   SMEM_PTR(sc.base); SMEM_PTR(KW);
   constexpr int QMAX = (1 << BITS) - 1;
   constexpr int HS = 8 / BITS;
+  constexpr int WLK = 16 * BITS / 8;  // K code words per lane per tile in the block
   const int g = lane >> 2, q = lane & 3;
   const int c0 = 16 * jb + 2 * q;
   const int slot0 = 2 * (jb % HS), wbase = 2 * (jb / HS);
@@ -936,11 +942,18 @@ __device__ __noinline__ void k_fix(const double* kparam64, const Scr sc, int jb,
     badm &= badm - 1;
     const int e = bit >> 1, pr = bit & 1;
     const int t = 16 * (e >> 1) + 8 * (e & 1) + g, ch = c0 + 8 * pr;
+    const int sh = (slot0 + pr) * BITS;
+    const int word = ((e >> 1) * 32 + lane) * WLK + (e & 1) + wbase;  // global word of the block
+    const int slot = fix ? atomicAdd(fixcnt, 1) : fixcap;
+    if (slot < fixcap) {
+      fix[slot] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ch << 39) |
+                  ((unsigned long long)word << 46) | ((unsigned long long)sh << 58);
+      continue;
+    }
     const double* mrow = p64 + (int64_t)sc.fidx()[t] * 128;
     const __half* xrow = xsrc + (int64_t)t * 128;
     const uint32_t pv = exact_code_p(xrow + ch, mrow + ch, kp + 128 + ch, kp + ch, QMAX) |
                         (exact_code_p(xrow + ch + 1, mrow + ch + 1, kp + 128 + ch + 1, kp + ch + 1, QMAX) << 16);
-    const int sh = (slot0 + pr) * BITS;
     const uint32_t clr = ~(((uint32_t)QMAX | ((uint32_t)QMAX << 16)) << sh);
     if constexpr (BITS == 2) {
       uint32_t* wp = &KW[((e >> 1) * 32 + lane) * 4 + (((e & 1) + wbase) ^ ((lane >> 3) & 3))];
@@ -1261,7 +1274,9 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         bar_sub(sgi);  // per-channel fp64 params in HBM
 #pragma unroll
         for (int jc = 0; jc < 2; ++jc)
-          if (badm[jc]) k_fix<BITS>(c.kparam64, sc, 2 * w + jc, lane, badm[jc], xsrc, p64, blk, KW, wreg, stats);
+          if (badm[jc])
+            k_fix<BITS>(c.kparam64, sc, 2 * w + jc, lane, badm[jc], xsrc, p64, blk, KW, wreg, stats, c.fix, c.fixcap,
+                        c.work + 2);
         if constexpr (BITS == 4) {  // word h + 2w of lane (tile tt) holds chunks 2w, 2w+1
           uint32_t* dst = reinterpret_cast<uint32_t*>(c.kcodes + blk * c.blk_bytes);
 #pragma unroll
@@ -1367,6 +1382,32 @@ encode_tc_kernel(const Args A, const __grid_constant__ CUtensorMap tmK, const __
   if (warp == 0) tmem_free<256>(tmem);
 }
 
+// Deferred K code fix-ups (k_fix): per entry the reference's fp64 code sequence for the two
+// elements of a pair (quant.py:103-109 via exact_code_at, the stored fp64 params and pattern
+// values) patched into the block's code word -- entries sharing a word touch disjoint bits.
+__global__ void kfix_kernel(DevCache c, const __half* src, int64_t unit_stride, int first_block) {
+  const int n = min(*reinterpret_cast<volatile int*>(c.work + 2), c.fixcap);
+  const int64_t row0 = c.blk_start[first_block];
+  const int qmax = (1 << c.bits) - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long en = c.fix[i];
+    const int64_t blk = (int64_t)(uint32_t)en;
+    const int t = (int)((en >> 32) & 127), ch = (int)((en >> 39) & 127), word = (int)((en >> 46) & 4095),
+              sh = (int)((en >> 58) & 31);
+    const int u = (int)(blk / c.NBcap), b = (int)(blk % c.NBcap);
+    const int pidx = c.kidx[blk * c.GP + t];
+    const __half* xrow = src + (int64_t)u * unit_stride + (c.blk_start[b] - row0 + t) * 128;
+    const double* mrow = c.kpat64 + ((int64_t)u * c.Pcap + pidx) * 128;
+    const double* kp = c.kparam64 + blk * 256;
+    const uint32_t pv = exact_code_at(xrow + ch, mrow + ch, kp[128 + ch], kp[ch], qmax) |
+                        (exact_code_at(xrow + ch + 1, mrow + ch + 1, kp[128 + ch + 1], kp[ch + 1], qmax) << 16);
+    uint32_t* wp = reinterpret_cast<uint32_t*>(c.kcodes + blk * c.blk_bytes) + word;
+    atomicAnd(wp, ~(((uint32_t)qmax | ((uint32_t)qmax << 16)) << sh));
+    atomicOr(wp, pv << sh);
+    if (c.stats) atomicAdd(&c.stats[1], 1u);
+  }
+}
+
 // TMA descriptor of a [U][rows][128] fp16 tensor (unit stride in elements), 64 x 128 x 1 boxes
 static bool make_tmap3(CUtensorMap* map, const void* base, uint64_t rows, uint64_t units, int64_t unit_stride) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1461,6 +1502,8 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
     cudaFuncSetAttribute(fe::encode_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, fe::smem_bytes(4));
     fe::encode_tc_kernel<4><<<grid, fe::NTHR, fe::smem_bytes(4), st>>>(a, tk, tv);
   }
+  if (c.fix && c.fixcap > 0)  // the deferred K code fix-ups (count on the device: grid-stride)
+    fe::kfix_kernel<<<4 * nsm, 256, 0, st>>>(c, k, unit_stride, first_block);
   return cudaGetLastError();
 }
 
