@@ -1092,7 +1092,7 @@ template <int BITS>
 __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, int blk_bytes, int64_t Tcap,
                                      const unsigned char* X, const float* M, Scr sc, int rb, int lane, int L, int u,
                                      int64_t start, int64_t blk, const __half* xsrc, const double* p64,
-                                     unsigned* stats) {
+                                     unsigned* stats, unsigned long long* fix, int fixcap, int* fixcnt) {
   SMEM_PTR(X); SMEM_PTR(M); SMEM_PTR(sc.base);
   constexpr int QMAX = (1 << BITS) - 1;
   constexpr int HS = 8 / BITS;
@@ -1128,7 +1128,8 @@ __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, in
 #pragma unroll
     for (int i = 0; i < 16; ++i) pp[i] = 0u;
   }
-  if (badm) {  // rare: the reference's fp64 sequence decides inside the guard band
+  if (badm) {  // rare: the reference's fp64 sequence decides inside the guard band (deferred to
+               // kfix_kernel through the fix list; in line when the list is full)
     const double* mr = flatten ? p64 + (int64_t)idx * 128 : nullptr;
     const __half* xrow = xsrc + (int64_t)t * 128;
     const double* vp = vparam64 + 2 * ((int64_t)u * Tcap + start + t);
@@ -1137,6 +1138,12 @@ __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, in
       const int i = __ffs(badm) - 1;
       badm &= badm - 1;
       const int ca = 16 * (i >> 1) + 8 * (i & 1) + 2 * q;
+      const int fs = fix ? atomicAdd(fixcnt, 1) : fixcap;
+      if (fs < fixcap) {  // V entry: block, token, first channel of the pair, side bit 63
+        fix[fs] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ca << 39) |
+                  (1ull << 63);
+        continue;
+      }
       const uint32_t pv = exact_code_p(xrow + ca, mr ? mr + ca : nullptr, vp + 1, vp, QMAX) |
                           (exact_code_p(xrow + ca + 1, mr ? mr + ca + 1 : nullptr, vp + 1, vp, QMAX) << 16);
 #pragma unroll
@@ -1287,7 +1294,8 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         __syncwarp();
 #pragma unroll 1
         for (int rs = 0; rs < 4; ++rs)
-          v_codes<BITS>(c.vcodes, c.vparam64, c.blk_bytes, c.Tcap, X, M, sc, 32 * w + 8 * rs, lane, L, u, start, blk, xsrc, p64, stats);
+          v_codes<BITS>(c.vcodes, c.vparam64, c.blk_bytes, c.Tcap, X, M, sc, 32 * w + 8 * rs, lane, L, u, start, blk, xsrc,
+                        p64, stats, c.fix, c.fixcap, c.work + 2);
       }
       // release the x tile; the last warp out takes the subgroup's next item (this chunk's
       // counter, else its static first item of the next chunk) and starts that span's TMA
@@ -1382,16 +1390,43 @@ encode_tc_kernel(const Args A, const __grid_constant__ CUtensorMap tmK, const __
   if (warp == 0) tmem_free<256>(tmem);
 }
 
-// Deferred K code fix-ups (k_fix): per entry the reference's fp64 code sequence for the two
-// elements of a pair (quant.py:103-109 via exact_code_at, the stored fp64 params and pattern
-// values) patched into the block's code word -- entries sharing a word touch disjoint bits.
-__global__ void kfix_kernel(DevCache c, const __half* src, int64_t unit_stride, int first_block) {
+// Deferred code fix-ups (k_fix, v_codes): per entry the reference's fp64 code sequence for the
+// two elements of a pair (quant.py:103-109 via exact_code_at, the stored fp64 params and pattern
+// values) patched into the block's code words -- entries sharing a word touch disjoint bits.
+__global__ void kfix_kernel(DevCache c, const __half* src, const __half* src_v, int64_t unit_stride, int first_block) {
   const int n = min(*reinterpret_cast<volatile int*>(c.work + 2), c.fixcap);
   const int64_t row0 = c.blk_start[first_block];
   const int qmax = (1 << c.bits) - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const unsigned long long en = c.fix[i];
     const int64_t blk = (int64_t)(uint32_t)en;
+    if (en >> 63) {  // V pair: token t, channels ca, ca + 1 (own params; RAW tokens code the raw row)
+      const int t = (int)((en >> 32) & 127), ca = (int)((en >> 39) & 127);
+      const int u = (int)(blk / c.NBcap), b = (int)(blk % c.NBcap);
+      const int64_t start = c.blk_start[b];
+      const int pidx = c.vidx[blk * c.GP + t];
+      const __half* xrow = src_v + (int64_t)u * unit_stride + (start - row0 + t) * 128;
+      const double* mrow = pidx >= 0 ? c.vpat64 + ((int64_t)u * c.Pcap + pidx) * 128 : nullptr;
+      const double* vp = c.vparam64 + 2 * ((int64_t)u * c.Tcap + start + t);
+      const int WL = frag_words_per_lane(c.Dp, c.bits);
+      uint8_t* tile = c.vcodes + blk * c.blk_bytes + (size_t)(t >> 4) * tile_bytes(c.Dp, c.bits);
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int ch = ca + k2;
+        const uint32_t code = exact_code_at(xrow + ch, mrow ? mrow + ch : nullptr, vp[1], vp[0], qmax);
+        // V^T fragment location of (channel ch, token t): side 1, row = ch & 15, col = t & 15
+        const int row = ch & 15, col = t & 15;
+        const int lane = 4 * (row & 7) + ((col & 7) >> 1), R = 4 * (ch >> 4) + (row >> 3) + 2 * (col >> 3);
+        int word, slot;
+        frag_word_slot(1, R, c.bits, word, slot);
+        const int sh = ((col & 1) ? 16 : 0) + slot * c.bits;
+        uint32_t* wp = reinterpret_cast<uint32_t*>(tile) + lane * WL + word;
+        atomicAnd(wp, ~((uint32_t)qmax << sh));
+        atomicOr(wp, code << sh);
+      }
+      if (c.stats) atomicAdd(&c.stats[1], 1u);
+      continue;
+    }
     const int t = (int)((en >> 32) & 127), ch = (int)((en >> 39) & 127), word = (int)((en >> 46) & 4095),
               sh = (int)((en >> 58) & 31);
     const int u = (int)(blk / c.NBcap), b = (int)(blk % c.NBcap);
@@ -1503,7 +1538,7 @@ cudaError_t launch_encode_tc(const DevCache& c, int max_p, const __half* k, cons
     fe::encode_tc_kernel<4><<<grid, fe::NTHR, fe::smem_bytes(4), st>>>(a, tk, tv);
   }
   if (c.fix && c.fixcap > 0)  // the deferred K code fix-ups (count on the device: grid-stride)
-    fe::kfix_kernel<<<4 * nsm, 256, 0, st>>>(c, k, unit_stride, first_block);
+    fe::kfix_kernel<<<4 * nsm, 256, 0, st>>>(c, k, v, unit_stride, first_block);
   return cudaGetLastError();
 }
 
