@@ -713,8 +713,9 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
     SpanSrc<T_> sv{(const T_*)v, T * c->D, 0, INT64_MAX / 4};
     cudaError_t e1 = cudaErrorNotSupported;
     if constexpr (std::is_same<T_, __half>::value) {
-      // deferred K code fix-up list: ~1e-3 of the elements at cfg2; an overflow is fixed in line
-      const int64_t want = std::min<int64_t>(std::max<int64_t>((int64_t)c->U * c->nb * 16, 1 << 16), 1 << 26);
+      // deferred code fix-up list (~0.25 pairs per token-unit at cfg2: 64 per block leaves 4x
+      // headroom); an overflow is fixed in line
+      const int64_t want = std::min<int64_t>(std::max<int64_t>((int64_t)c->U * c->nb * 64, 1 << 16), 1 << 27);
       if (c->dev.fixcap < want) {
         if (c->dev.fix) cudaFree(c->dev.fix);
         c->dev.fix = nullptr;

@@ -919,20 +919,19 @@ __device__ __noinline__ uint32_t k_pass(const unsigned char* X, const float* M, 
   }
   return badm;
 }
-// guard-band pairs of chunk jb (bits of badm): deferred to kfix_kernel through the cache's fix
-// list (word and shift of the pair in the block's global code words + its position), so the
-// fp64 reference sequence with its L2 reads of x, the pattern value and the params runs after
-// the encoder instead of on an item's critical path (a K item's fix-ups and the barrier waiting
-// for the warp with the most were ~1/4 of its time); in line (exact, from the stored fp64
-// params) only when the list is full.
+// Guard-band pairs of chunk jb (bits of badm).  The common route defers them to kfix_kernel
+// (k_defer below, in line at the call site); this exact in-line fix runs only for pairs the
+// full fix list could not take.  2 bits: into the shared code words KW before they are copied
+// out; 4 bits: into the lane's own global code words right after it stored them (the register
+// words are never passed by pointer -- that put them in local memory for the whole K pass).
 template <int BITS>
 __device__ __noinline__ void k_fix(const double* kparam64, const Scr sc, int jb, int lane, uint32_t badm,
-                                   const __half* xsrc, const double* p64, int64_t blk, uint32_t* KW, uint32_t* wreg,
-                                   unsigned* stats, unsigned long long* fix, int fixcap, int* fixcnt) {
-  SMEM_PTR(sc.base); SMEM_PTR(KW);
+                                   const __half* xsrc, const double* p64, int64_t blk, uint32_t* KW, uint32_t* gw,
+                                   unsigned* stats) {
+  SMEM_PTR(sc.base);
   constexpr int QMAX = (1 << BITS) - 1;
   constexpr int HS = 8 / BITS;
-  constexpr int WLK = 16 * BITS / 8;  // K code words per lane per tile in the block
+  constexpr int WLK = 16 * BITS / 8;
   const int g = lane >> 2, q = lane & 3;
   const int c0 = 16 * jb + 2 * q;
   const int slot0 = 2 * (jb % HS), wbase = 2 * (jb / HS);
@@ -942,29 +941,40 @@ __device__ __noinline__ void k_fix(const double* kparam64, const Scr sc, int jb,
     badm &= badm - 1;
     const int e = bit >> 1, pr = bit & 1;
     const int t = 16 * (e >> 1) + 8 * (e & 1) + g, ch = c0 + 8 * pr;
-    const int sh = (slot0 + pr) * BITS;
-    const int word = ((e >> 1) * 32 + lane) * WLK + (e & 1) + wbase;  // global word of the block
-    const int slot = fix ? atomicAdd(fixcnt, 1) : fixcap;
-    if (slot < fixcap) {
-      fix[slot] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ch << 39) |
-                  ((unsigned long long)word << 46) | ((unsigned long long)sh << 58);
-      continue;
-    }
     const double* mrow = p64 + (int64_t)sc.fidx()[t] * 128;
     const __half* xrow = xsrc + (int64_t)t * 128;
     const uint32_t pv = exact_code_p(xrow + ch, mrow + ch, kp + 128 + ch, kp + ch, QMAX) |
                         (exact_code_p(xrow + ch + 1, mrow + ch + 1, kp + 128 + ch + 1, kp + ch + 1, QMAX) << 16);
+    const int sh = (slot0 + pr) * BITS;
     const uint32_t clr = ~(((uint32_t)QMAX | ((uint32_t)QMAX << 16)) << sh);
-    if constexpr (BITS == 2) {
-      uint32_t* wp = &KW[((e >> 1) * 32 + lane) * 4 + (((e & 1) + wbase) ^ ((lane >> 3) & 3))];
-      atomicAnd(wp, clr);
-      atomicOr(wp, pv << sh);
-    } else {
-#pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) wreg[k2] = k2 == e ? ((wreg[k2] & clr) | (pv << sh)) : wreg[k2];
-    }
+    uint32_t* wp = BITS == 2 ? &KW[((e >> 1) * 32 + lane) * 4 + (((e & 1) + wbase) ^ ((lane >> 3) & 3))]
+                             : gw + ((e >> 1) * 32 + lane) * WLK + (e & 1) + wbase;
+    atomicAnd(wp, clr);
+    atomicOr(wp, pv << sh);
     if (stats) atomicAdd(&stats[1], 1u);
   }
+}
+// the deferral itself: one 64-bit entry per pair (block, token, channel, global word, shift),
+// one slot each from the cache's counter; returns the pairs the full list did not take
+template <int BITS>
+__device__ __forceinline__ uint32_t k_defer(uint32_t badm, int jb, int lane, int64_t blk, unsigned long long* fix,
+                                            int fixcap, int* fixcnt) {
+  constexpr int HS = 8 / BITS;
+  constexpr int WLK = 16 * BITS / 8;
+  const int g = lane >> 2, q = lane & 3;
+  const int slot0 = 2 * (jb % HS), wbase = 2 * (jb / HS);
+  while (badm) {
+    const int bit = __ffs(badm) - 1;
+    const int slot = fix ? atomicAdd(fixcnt, 1) : fixcap;
+    if (slot >= fixcap) return badm;
+    badm &= badm - 1;
+    const int e = bit >> 1, pr = bit & 1;
+    const int t = 16 * (e >> 1) + 8 * (e & 1) + g, ch = 16 * jb + 2 * q + 8 * pr;
+    const int word = ((e >> 1) * 32 + lane) * WLK + (e & 1) + wbase;
+    fix[slot] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ch << 39) |
+                ((unsigned long long)word << 46) | ((unsigned long long)((slot0 + pr) * BITS) << 58);
+  }
+  return 0u;
 }
 // groups of chunk jb with several elements inside the fp32 error window: exact fp64 extrema
 // over the window, stored as double halves in (kmx, xmx) / (kmn, xmn) with info = 1 << 16.
@@ -1279,15 +1289,20 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         bar_sub(sgi);  // per-channel statistics of all 128 channels
         k_scalar<BITS>(A, X, M, pt, sc, st, L, p64, blk, stats);
         bar_sub(sgi);  // per-channel fp64 params in HBM
+        uint32_t ovf[2];
 #pragma unroll
-        for (int jc = 0; jc < 2; ++jc)
-          if (badm[jc])
-            k_fix<BITS>(c.kparam64, sc, 2 * w + jc, lane, badm[jc], xsrc, p64, blk, KW, wreg, stats, c.fix, c.fixcap,
-                        c.work + 2);
-        if constexpr (BITS == 4) {  // word h + 2w of lane (tile tt) holds chunks 2w, 2w+1
-          uint32_t* dst = reinterpret_cast<uint32_t*>(c.kcodes + blk * c.blk_bytes);
+        for (int jc = 0; jc < 2; ++jc) ovf[jc] = k_defer<BITS>(badm[jc], 2 * w + jc, lane, blk, c.fix, c.fixcap, c.work + 2);
+        uint32_t* gw = reinterpret_cast<uint32_t*>(c.kcodes + blk * c.blk_bytes);
+        if constexpr (BITS == 2) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) dst[((e >> 1) * 32 + lane) * 8 + (e & 1) + 2 * w] = wreg[e];
+          for (int jc = 0; jc < 2; ++jc)
+            if (ovf[jc]) k_fix<BITS>(c.kparam64, sc, 2 * w + jc, lane, ovf[jc], xsrc, p64, blk, KW, gw, stats);
+        } else {  // word h + 2w of lane (tile tt) holds chunks 2w, 2w+1
+#pragma unroll
+          for (int e = 0; e < 16; ++e) gw[((e >> 1) * 32 + lane) * 8 + (e & 1) + 2 * w] = wreg[e];
+#pragma unroll
+          for (int jc = 0; jc < 2; ++jc)
+            if (ovf[jc]) k_fix<BITS>(c.kparam64, sc, 2 * w + jc, lane, ovf[jc], xsrc, p64, blk, KW, gw, stats);
         }
       } else {
         v_scalar<BITS>(A, X, M, pt, sc, st, L, start, u, blk, p64, stats);
