@@ -963,16 +963,27 @@ __device__ __forceinline__ uint32_t k_defer(uint32_t badm, int jb, int lane, int
   constexpr int WLK = 16 * BITS / 8;
   const int g = lane >> 2, q = lane & 3;
   const int slot0 = 2 * (jb % HS), wbase = 2 * (jb / HS);
+  // slots: one atomic per warp for all of its lanes' pairs (every lane calls)
+  const int n = __popc(badm);
+  if (!__any_sync(0xffffffffu, n != 0)) return 0u;
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int base = 0;
+  if (lane == 31) base = fix ? atomicAdd(fixcnt, incl) : fixcap;
+  int slot = __shfl_sync(0xffffffffu, base, 31) + incl - n;
   while (badm) {
     const int bit = __ffs(badm) - 1;
-    const int slot = fix ? atomicAdd(fixcnt, 1) : fixcap;
     if (slot >= fixcap) return badm;
     badm &= badm - 1;
     const int e = bit >> 1, pr = bit & 1;
     const int t = 16 * (e >> 1) + 8 * (e & 1) + g, ch = 16 * jb + 2 * q + 8 * pr;
     const int word = ((e >> 1) * 32 + lane) * WLK + (e & 1) + wbase;
-    fix[slot] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ch << 39) |
-                ((unsigned long long)word << 46) | ((unsigned long long)((slot0 + pr) * BITS) << 58);
+    fix[slot++] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ch << 39) |
+                  ((unsigned long long)word << 46) | ((unsigned long long)((slot0 + pr) * BITS) << 58);
   }
   return 0u;
 }
