@@ -715,8 +715,10 @@ extern "C" int pkv_prefill(pkv_cache* c, const void* k, const void* v, int64_t T
     if constexpr (std::is_same<T_, __half>::value) {
       // deferred code fix-up list (~0.25 pairs per token-unit at cfg2: 64 per block leaves 4x
       // headroom); an overflow is fixed in line
-      const int64_t want = std::min<int64_t>(std::max<int64_t>((int64_t)c->U * c->nb * 64, 1 << 16), 1 << 27);
-      if (c->dev.fixcap < want) {
+      int64_t want = std::min<int64_t>(std::max<int64_t>((int64_t)c->U * c->nb * 64, 1 << 16), 1 << 27);
+      const char* fcap = getenv("PKV_FIX_CAP");  // tests: a tiny list exercises the in-line fix
+      if (fcap) want = std::max<int64_t>(atoll(fcap), 1);
+      if (c->dev.fixcap < want || (fcap && c->dev.fixcap != want)) {
         if (c->dev.fix) cudaFree(c->dev.fix);
         c->dev.fix = nullptr;
         c->dev.fixcap = 0;

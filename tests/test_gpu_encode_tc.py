@@ -87,3 +87,30 @@ def test_encode_tc_heavy_ties(pkv, monkeypatch):
         if name in a:
             assert torch.equal(a[name], b[name]), name
     print("tc stats:", a["stats"])
+
+
+@pytest.mark.parametrize("cap,heavy", [(3, False), (3, True), (1000, True)])
+def test_encode_tc_fix_list_overflow(pkv, monkeypatch, cap, heavy):
+    """Guard-band code fix-ups normally go to kfix_kernel through the cache's fix list; a list
+    too small for them (PKV_FIX_CAP) sends the rest down the in-line exact path.  Either way
+    every arena equals K1's bit for bit (2 and 4 bits)."""
+    from paper_2510_05176_b200.config import EngineConfig
+    from paper_2510_05176_b200.synth import synth_kv
+
+    U, T = 4, 1536
+    if heavy:
+        g = torch.Generator(device="cuda").manual_seed(12)
+        k = torch.randint(-3, 4, (U, T, 128), generator=g, device="cuda").half() * 0.5
+        v = torch.randint(-2, 3, (U, T, 128), generator=g, device="cuda").half()
+    else:
+        k, v = synth_kv(U, T, 128, seed=21)
+    for bits in (2, 4):
+        cfg = EngineConfig(bits=bits, pattern_count=32)
+        monkeypatch.setenv("PKV_FIX_CAP", str(cap))
+        a = _run(pkv, monkeypatch, True, cfg, k, v, diag=True)
+        monkeypatch.delenv("PKV_FIX_CAP")
+        b = _run(pkv, monkeypatch, False, cfg, k, v, diag=True)
+        for name, _ in ARENAS:
+            if name in a:
+                assert torch.equal(a[name], b[name]), (bits, name)
+        assert a["stats"][1] > cap, "the data must need more fix-ups than the list holds"
