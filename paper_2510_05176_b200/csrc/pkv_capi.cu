@@ -839,7 +839,8 @@ static int attn_impl(pkv_cache* c, const float* q, int32_t gqa, float sm_scale, 
   a.blk0 = blk0; a.nb = blk1 - blk0; a.ml = ml;
   // enough CTAs for ~4 waves (K3-TC: 4 CTAs/SM at GQA <= 4, 2 CTAs of two head halves above),
   // >= 4 blocks per chunk (one per warp)
-  const int target = (gqa <= 4 ? 16 : 8) * num_sms;
+  static const char* tenv = getenv("PKV_ATTN_CTAS_PER_SM");  // tuning: CTAs per SM the chunking aims at
+  const int target = (tenv ? std::max(1, atoi(tenv)) : (gqa <= 4 ? 16 : 8)) * num_sms;
   int nchunk = std::max(1, std::min((target + c->U - 1) / c->U, (a.nb + 3) / 4));
   nchunk = std::max(nchunk, (a.nb + 255) / 256);  // K3-TC: <= 256 blocks per chunk (s32 digit sums)
   a.bpc = std::max(1, (a.nb + nchunk - 1) / nchunk);
