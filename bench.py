@@ -325,7 +325,7 @@ def leg_encode(ctx, bits: int, k, v, pool_patterns, results, want_e2e: bool):
     bpt = enc_bytes_per_token(bits)
     enc_bytes = U * committed * bpt
     r = dict(enc_ms=enc_ms, kern_ms=kern_ms, enc_gbps=ctx.world * enc_bytes / (enc_ms * 1e-3) / 1e9, bpt=bpt,
-             enc_bytes=enc_bytes, mine_ms=mine_ms, clk=clk, launches=2 * args.steps, info=cache.info())
+             enc_bytes=enc_bytes, mine_ms=mine_ms, clk=clk, launches=3 * args.steps, info=cache.info())
 
     # ---- decode attention over the encoded cache -----------------------------------------
     q = torch.randn((U, args.gqa, D), device="cuda", dtype=torch.float32)
@@ -919,7 +919,7 @@ def main():
                         "installed pattern tables as in `value`; the encoded cache stays device-resident (its "
                         "consumer is decode attention), the step's result read back is each unit's codes of the "
                         "last committed token"},
-        "gpu_launches": r["launches"],
+        "gpu_launches": r["launches"],  # per step: encode_tc_kernel + kfix_kernel + window_put_kernel
         "clocks": r["clk"],
     }
     if "decode_loop" in r:
