@@ -469,8 +469,9 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
       st_wait();
       fence_proxy_async();
       tc_fence_before();
-      // QK(b + 1) as soon as every warp's A_K rows are in: warp 0 waits, the others only arrive
-      if (warp == 0) {
+      // QK(b + 1) as soon as every warp's A_K rows are in: the last warp waits and issues (warp
+      // 0 issues PV / W), the others only arrive
+      if (warp == NT / 32 - 1) {
         asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
         if (lane == 0) {
           tc_fence_after();
