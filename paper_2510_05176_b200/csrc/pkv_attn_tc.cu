@@ -288,8 +288,15 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
   float s_nx = 0.f;      // K scale of channel tq (block b + 1)
   int kidx_t = RAW, vidx_t = RAW, kidx_n = RAW, vidx_n = RAW, L_t = 128, L_n = 128;
   float vs_t = 0.f, vz_t = 0.f, vs_n = 0.f, vz_n = 0.f;
-  auto load_k = [&](int bb) {
-    const uint8_t* p = klane + (uint32_t)bb * bbytes;
+  // the blocks load in order (K two ahead, V and metadata one ahead): running pointers
+  const uint8_t* kptr = klane + (size_t)b0 * bbytes;
+  const float* sptr = ks_u + (size_t)b0 * kps;
+  const uint8_t* vptr = vlane + (size_t)b0 * bbytes;
+  const int* lptr = c.blk_len + b0;
+  uint32_t mo = (uint32_t)b0 * gp;
+  auto load_k = [&]() {
+    const uint8_t* p = kptr;
+    kptr += bbytes;
 #pragma unroll
     for (int i = 0; i < KT; ++i) {
       if (ntile == 8 || kt0 + i < ntile) {
@@ -303,10 +310,12 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
         for (int j = 0; j < NWK; ++j) kw[i][j] = 0u;
       }
     }
-    s_nx = __ldg(ks_u + (uint32_t)bb * kps);
+    s_nx = __ldg(sptr);
+    sptr += kps;
   };
-  auto load_v = [&](int bb) {
-    const uint8_t* p = vlane + (uint32_t)bb * bbytes;
+  auto load_v = [&]() {
+    const uint8_t* p = vptr;
+    vptr += bbytes;
     if (ntile == 8) {
 #pragma unroll
       for (int ti = 0; ti < VT; ++ti) vw[ti] = __ldg(reinterpret_cast<const uint2*>(p + ti * TB));
@@ -316,10 +325,11 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
         vw[ti] = vt0 + ti < ntile ? __ldg(reinterpret_cast<const uint2*>(p + ti * TB)) : make_uint2(0u, 0u);
     }
   };
-  auto load_meta = [&](int bb) {  // token tq of block bb -> the *_n registers
-    L_n = __ldg(c.blk_len + bb);
+  auto load_meta = [&]() {  // token tq of the next block -> the *_n registers
+    L_n = __ldg(lptr++);
+    const uint32_t o = mo;
+    mo += gp;
     if (has_slot) {
-      const uint32_t o = (uint32_t)bb * gp;
       kidx_n = __ldg(kidx_u + o);
       vidx_n = __ldg(vidx_u + o);
       const float2 vp = __ldg(vp_u + o);
@@ -361,6 +371,7 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
   bool fresh = true;
   const int vsh = vshift<BITS>(tq);
   const int kposv = kpos_v(tq);
+  const int oh_base = (kposv >> 4) * 2048 + (kposv & 15);  // this token's byte in a one-hot tile
   int oh_off = -1;  // this token's one-hot byte (cleared after the block's W MMA; head half 0)
   // descriptors (thread 0 issues every MMA)
   const uint64_t dqk = desc_none(bqk, 128, 2048), dpv = desc_none(bpv, 128, 2048), dbw = desc_none(bw, 128, 2048);
@@ -407,12 +418,12 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
 
   __syncthreads();  // block statistics
   if (nit > 0) {
-    load_k(b0);
-    load_v(b0);
-    load_meta(b0);
+    load_k();
+    load_v();
+    load_meta();
     next_meta();
     k_side(0);
-    if (nit > 1) load_k(b0 + 1);
+    if (nit > 1) load_k();
     st_wait();
     fence_proxy_async();
     tc_fence_before();
@@ -427,7 +438,6 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
 
   // ---- block loop: QK(b) was issued by the previous iteration --------------------------------
   for (int it = 0; it < nit; ++it) {
-    const int b = b0 + it;
     const bool more = it + 1 < nit;
     // (i) scores of token tq, heads h0 .. h0 + 3
     float lg[4];
@@ -486,8 +496,8 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
       // all of the iteration's global loads go out here and in (iv): every load shares one
       // scoreboard, so metadata issued at the top of the loop made the next K-side read (the
       // first consumer) wait for loads just issued (measured 0.600 -> 0.659 ms, here 0.582)
-      load_meta(b + 1);
-      if (it + 2 < nit) load_k(b + 2);
+      load_meta();
+      if (it + 2 < nit) load_k();
     }
     // (iii) softmax of token tq: p' = 2^31 exp2(lg - m_ref), digits of p' and p' s_t 2^(Ev-31)
     // (lg[0] > -inf marks a valid token: head h0 < G always, NG = 8 only serves G > 4)
@@ -544,10 +554,10 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
         st16x128x4(T + lrow + (16u << 16) + cav, rb);
       }
     }
-    if (more) load_v(b + 1);
+    if (more) load_v();
     if (hh == 0) {
       if (oh_off >= 0) onehot[oh_off] = 0;
-      oh_off = (lg[0] > -INFINITY && vidx_t >= 0 && vidx_t < Pv) ? (vidx_t >> 7) * 16384 + (kposv >> 4) * 2048 + (vidx_t & 127) * 16 + (kposv & 15) : -1;
+      oh_off = (lg[0] > -INFINITY && vidx_t >= 0 && vidx_t < Pv) ? (vidx_t >> 7) * 16384 + (vidx_t & 127) * 16 + oh_base : -1;
       if (oh_off >= 0) onehot[oh_off] = 1;
     }
     auto write_rows = [&]() {
