@@ -499,58 +499,244 @@ __global__ void __launch_bounds__(ATT_THREADS, NT == 1 ? 4 : 2) attn_chunk_kerne
 }
 
 // merge: exact fp32 attention over the window rows + combine chunk partials.
-// grid U, block 32*G threads (warp = head).
+// grid U, block 32*G threads.  The window is shared by the unit's G query heads and every row is
+// read from HBM once per unit: (1) thread per window row scores it against all G queries (the
+// row's loads are all issued before the first FMA, so a row costs one HBM latency, not D), (2)
+// warp h takes the max / exp2 / sum of head h's scores, (3) warp w accumulates p_r v_r for all G
+// heads over rows r = w (mod G) with lanes over 4-channel vectors, 8 rows in flight, (4) warp h
+// sums the G per-warp partials of head h in a fixed order (deterministic) and LSE-combines the
+// chunk partials.  VEC needs D % 4 == 0 (4-element vector loads); otherwise scalar loads.
+// (A warp per head walking the rows with a 5-shuffle reduction and an online rescale per row cost
+// ~12% of a cfg2 decode step; a thread-per-row variant with scalar loads was no faster.)
 template <typename T>
+struct Vec4 { using raw = uint2; };
+template <> struct Vec4<float> { using raw = uint4; };
+template <> struct Vec4<double> { struct raw { uint4 a, b; }; };
+template <typename T>
+__device__ __forceinline__ typename Vec4<T>::raw ld4(const T* p) {
+  return __ldg(reinterpret_cast<const typename Vec4<T>::raw*>(p));
+}
+template <>
+__device__ __forceinline__ Vec4<double>::raw ld4<double>(const double* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  return {__ldg(q), __ldg(q + 1)};
+}
+__device__ __forceinline__ float4 cvt4(uint2 r, const __half*) {
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 cvt4(uint2 r, const __nv_bfloat16*) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 cvt4(uint4 r, const float*) {
+  return make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
+}
+__device__ __forceinline__ float4 cvt4(Vec4<double>::raw r, const double*) {
+  const double2 a = *reinterpret_cast<const double2*>(&r.a), b = *reinterpret_cast<const double2*>(&r.b);
+  return make_float4((float)a.x, (float)a.y, (float)b.x, (float)b.y);
+}
+template <typename T>
+__device__ __forceinline__ float to_f32(T x) { return (float)to_f64(x); }
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half x) { return __half2float(x); }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <typename T, bool VEC, int GC>
 __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_slot0, float* out) {
-  const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (h >= a.G) return;
-  const int D = c.D, Dp = c.Dp;
-  const float* q = a.q + ((int64_t)u * a.G + h) * D;
-  float qv[4];
+  extern __shared__ float msm[];
+  constexpr int GM = GC > 0 ? GC : MAXG;  // compile-time head count (GC = 0: a.G at run time)
+  const int u = blockIdx.x, G = GC > 0 ? GC : a.G, NTH = 32 * G;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int D = c.D, Dp = c.Dp, Wcap = c.Wcap;
+  float* qs = msm;                 // [G][D] queries
+  float* sc = qs + G * D;          // [G][Wcap] scores, then probabilities
+  float* red = sc + G * Wcap;      // [G warps][G heads][D] partial outputs (VEC)
+  for (int i = tid; i < G * D; i += NTH) qs[i] = a.q[(int64_t)u * G * D + i];
+  __syncthreads();
+  const T* wk = reinterpret_cast<const T*>(c.wk) + (int64_t)u * Wcap * D;
+  const T* wv = reinterpret_cast<const T*>(c.wv) + (int64_t)u * Wcap * D;
+  // (1) scores: thread per window row, all G heads
+  for (int r = tid; r < win_len; r += NTH) {
+    const int slot = win_slot0 + r;  // ring slot: win_slot0 < Wcap and r < Wcap
+    const T* kr = wk + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D;
+    float acc[GM];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) qv[j] = (lane + 32 * j < D) ? q[lane + 32 * j] : 0.f;
-  float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
-  const T* wk = reinterpret_cast<const T*>(c.wk) + (int64_t)u * c.Wcap * D;
-  const T* wv = reinterpret_cast<const T*>(c.wv) + (int64_t)u * c.Wcap * D;
-  for (int r = 0; r < win_len; ++r) {
-    const int64_t row = (int64_t)((win_slot0 + r) % c.Wcap) * D;
-    float s = 0.f;
+    for (int g = 0; g < GM; ++g) acc[g] = 0.f;
+    if constexpr (VEC) {
+      constexpr int NB = 16;       // 4-element vectors in flight per batch
+      for (int d0 = 0; d0 < D; d0 += 4 * NB) {
+        typename Vec4<T>::raw kv[NB];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) s = fmaf(qv[j], (float)to_f64(wk[row + lane + 32 * j]), s);
-    s = warp_sum_f(s) * a.scale_log2;
-    const float mn = fmaxf(m, s);
-    const float al = m == -INFINITY ? 0.f : exp2f(m - mn);
-    const float p = exp2f(s - mn);
-    l = l * al + p;
+        for (int j = 0; j < NB; ++j)
+          if (d0 + 4 * j < D) kv[j] = ld4(kr + d0 + 4 * j);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = o[j] * al + (lane + 32 * j < D ? p * (float)to_f64(wv[row + lane + 32 * j]) : 0.f);
-    m = mn;
+        for (int j = 0; j < NB; ++j) {
+          if (d0 + 4 * j >= D) break;
+          const float4 k4 = cvt4(kv[j], (const T*)nullptr);
+#pragma unroll
+          for (int g = 0; g < GM; ++g) {
+            if (g >= G) break;
+            const float4 q4 = *reinterpret_cast<const float4*>(qs + g * D + d0 + 4 * j);
+            acc[g] = fmaf(q4.x, k4.x, fmaf(q4.y, k4.y, fmaf(q4.z, k4.z, fmaf(q4.w, k4.w, acc[g]))));
+          }
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int d = 0; d < D; ++d) {
+        const float kv = to_f32(kr[d]);
+#pragma unroll
+        for (int g = 0; g < GM; ++g)
+          if (g < G) acc[g] = fmaf(qs[g * D + d], kv, acc[g]);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < GM; ++g)
+      if (g < G) sc[g * Wcap + r] = acc[g] * a.scale_log2;
   }
-  // combine with chunk partials
+  __syncthreads();
+  // (2) warp h = w: running max, probabilities, sum (log2 units)
+  const int h = w;
+  float* sh = sc + h * Wcap;
+  float m = -INFINITY;
+  for (int r = lane; r < win_len; r += 32) m = fmaxf(m, sh[r]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float l = 0.f;
+  for (int r = lane; r < win_len; r += 32) {
+    const float p = exp2f(sh[r] - m);
+    sh[r] = p;
+    l += p;
+  }
+  l = warp_sum_f(l);
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (VEC) {
+    __syncthreads();
+    // (3) warp w: rows r = w (mod G), all heads, lane = channels 4*lane .. 4*lane+3
+    float acc[GM][4];
+#pragma unroll
+    for (int g = 0; g < GM; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[g][j] = 0.f;
+    const bool on = 4 * lane < D;
+    constexpr int RB = 8;
+    for (int r0 = w; r0 < win_len; r0 += RB * G) {
+      typename Vec4<T>::raw vv[RB];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int r = r0 + i * G;
+        const int slot = win_slot0 + r;
+        if (on && r < win_len) vv[i] = ld4(wv + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D + 4 * lane);
+      }
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int r = r0 + i * G;
+        if (r >= win_len) break;
+        const float4 v4 = on ? cvt4(vv[i], (const T*)nullptr) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < GM; ++g) {
+          if (g >= G) break;
+          const float p = sc[g * Wcap + r];
+          acc[g][0] = fmaf(p, v4.x, acc[g][0]);
+          acc[g][1] = fmaf(p, v4.y, acc[g][1]);
+          acc[g][2] = fmaf(p, v4.z, acc[g][2]);
+          acc[g][3] = fmaf(p, v4.w, acc[g][3]);
+        }
+      }
+    }
+    if (on) {
+#pragma unroll
+      for (int g = 0; g < GM; ++g)
+        if (g < G)
+          *reinterpret_cast<float4*>(red + ((int64_t)w * G + g) * D + 4 * lane) =
+              make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+    }
+    __syncthreads();
+    if (on)
+      for (int ww = 0; ww < G; ++ww) {
+        const float4 x = *reinterpret_cast<const float4*>(red + ((int64_t)ww * G + h) * D + 4 * lane);
+        o[0] += x.x; o[1] += x.y; o[2] += x.z; o[3] += x.w;
+      }
+  } else {
+    __syncwarp();
+    // (3) o = sum_r p_r v_r for head h, lanes over channels
+#pragma unroll 2
+    for (int r = 0; r < win_len; ++r) {
+      const int slot = win_slot0 + r;
+      const T* vr = wv + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D;
+      const float p = sh[r];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lane + 32 * j < D) o[j] = fmaf(p, to_f32(vr[lane + 32 * j]), o[j]);
+    }
+  }
+  // channel of o[j]: VEC 4*lane + j, else lane + 32*j
+  auto chan = [&](int j) { return VEC ? 4 * lane + j : lane + 32 * j; };
+  // (4) combine with chunk partials (written by the chunk grid this launch depends on)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int ch = 0; ch < a.nchunk; ++ch) {
-    const float* pp = a.part + (((int64_t)u * a.nchunk + ch) * a.G + h) * (Dp + 2);
+    const float* pp = a.part + (((int64_t)u * a.nchunk + ch) * G + h) * (Dp + 2);
     const float pm = pp[Dp], pl = pp[Dp + 1];
     if (pm == -INFINITY) continue;
     const float mn = fmaxf(m, pm);
     const float al = m == -INFINITY ? 0.f : exp2f(m - mn), be = exp2f(pm - mn);
     l = l * al + pl * be;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = o[j] * al + (lane + 32 * j < Dp ? pp[lane + 32 * j] * be : 0.f);
+    for (int j = 0; j < 4; ++j) o[j] = o[j] * al + (chan(j) < Dp ? pp[chan(j)] * be : 0.f);
     m = mn;
   }
-  float* dst = out + ((int64_t)u * a.G + h) * D;
+  float* dst = out + ((int64_t)u * G + h) * D;
   if (a.ml) {  // partial (o, m, l) for a cross-rank LSE merge: m in natural-log units
 #pragma unroll
-    for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) dst[lane + 32 * j] = o[j];
+    for (int j = 0; j < 4; ++j) if (chan(j) < D) dst[chan(j)] = o[j];
     if (lane == 0) {
-      a.ml[((int64_t)u * a.G + h) * 2] = m * 0.6931471805599453f;
-      a.ml[((int64_t)u * a.G + h) * 2 + 1] = l;
+      a.ml[((int64_t)u * G + h) * 2] = m * 0.6931471805599453f;
+      a.ml[((int64_t)u * G + h) * 2 + 1] = l;
     }
     return;
   }
   const float inv = 1.f / l;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) if (lane + 32 * j < D) dst[lane + 32 * j] = o[j] * inv;
+  for (int j = 0; j < 4; ++j) if (chan(j) < D) dst[chan(j)] = o[j] * inv;
+}
+
+template <typename T, bool VEC, int GC>
+static cudaError_t launch_merge(const DevCache& c, const AttnArgs& a, int win_len, int win_slot0, float* out,
+                                cudaStream_t st) {
+  const size_t msmem = ((size_t)a.G * c.D + (size_t)a.G * c.Wcap + (VEC ? (size_t)a.G * a.G * c.D : 0)) * 4;
+  if (msmem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(attn_merge_kernel<T, VEC, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)msmem);
+    if (e != cudaSuccess) return e;
+  }
+  // programmatic dependent launch after a chunk grid: phases (1)-(3) read only the window and
+  // the queries (written before the chunk grid started) and overlap the chunk grid's tail;
+  // griddepcontrol.wait precedes the partials
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c.U);
+  cfg.blockDim = dim3(32 * a.G);
+  cfg.dynamicSmemBytes = msmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = a.nchunk > 0 ? 1 : 0;  // no chunk grid: the predecessor may be the window writer
+  return cudaLaunchKernelEx(&cfg, attn_merge_kernel<T, VEC, GC>, c, a, win_len, win_slot0, out);
+}
+
+template <typename T, bool VEC>
+static cudaError_t launch_merge_g(const DevCache& c, const AttnArgs& a, int win_len, int win_slot0, float* out,
+                                  cudaStream_t st) {
+  switch (a.G) {
+    case 4: return launch_merge<T, VEC, 4>(c, a, win_len, win_slot0, out, st);
+    case 8: return launch_merge<T, VEC, 8>(c, a, win_len, win_slot0, out, st);
+    default: return launch_merge<T, VEC, 0>(c, a, win_len, win_slot0, out, st);
+  }
 }
 
 size_t attn_smem_bytes(int Dp, int Pk, int Pv, int bits, int NT) {
@@ -593,8 +779,8 @@ cudaError_t launch_attn(const DevCache& c, const AttnArgs& a, int Pk_max, int Pv
   }
   AttnArgs a2 = a;
   if (a.nb == 0) a2.nchunk = 0;
-  attn_merge_kernel<T><<<c.U, 32 * a.G, 0, st>>>(c, a2, win_len, win_slot0, out);
-  return cudaGetLastError();
+  return c.D % 4 == 0 ? launch_merge_g<T, true>(c, a2, win_len, win_slot0, out, st)
+                      : launch_merge_g<T, false>(c, a2, win_len, win_slot0, out, st);
 }
 template cudaError_t launch_attn<__half>(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);
 template cudaError_t launch_attn<__nv_bfloat16>(const DevCache&, const AttnArgs&, int, int, int, int, float*, cudaStream_t);

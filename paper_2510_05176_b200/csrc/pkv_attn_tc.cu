@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(32 * NG, NG == 4 ? 4 : 2) attn_tc_kernel(DevCa
   constexpr int VT = 8 / HH;                 // V tiles per warp per block
   constexpr uint32_t ID_QK = idesc_i8(128, N, 0, 1, 0, 1);
   constexpr uint32_t ID_PV = idesc_i8(128, N, 0, 0, 0, 1);
+  // the window merge (attn_merge_kernel, launched programmatically dependent) may start its
+  // window rows once every chunk CTA is resident; it waits for this grid before the partials
+  asm volatile("griddepcontrol.launch_dependents;");
   const int u = blockIdx.y, chunk = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tq = HH == 1 ? tid : tid & 127, hh = HH == 1 ? 0 : tid >> 7, wq = HH == 1 ? warp : warp & 3;

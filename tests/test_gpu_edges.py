@@ -171,10 +171,11 @@ def test_bf16_fp32_inputs_prefill_decode(pkv, tdt):
     _attention_close(pkv, cache, U, d)
 
 
-@pytest.mark.parametrize("d,bits,gqa", [(64, 2, 4), (96, 4, 8), (40, 2, 2)])
+@pytest.mark.parametrize("d,bits,gqa", [(64, 2, 4), (96, 4, 8), (40, 2, 2), (42, 4, 3)])
 def test_small_head_dims(pkv, d, bits, gqa):
     """head_dim < 128: Dp = 64 (the KT = 4 attention kernel) or padded channels (96 -> 128,
-    40 -> 64); fp16 caches off the K1-TC envelope, bit-exact vs the oracle, attention 1e-3."""
+    40 -> 64, 42 -> 64: the window merge's scalar-load path, D % 4 != 0, and a run-time head
+    count); fp16 caches off the K1-TC envelope, bit-exact vs the oracle, attention 1e-3."""
     from paper_2510_05176_b200.config import EngineConfig
 
     U, T, S = 2, 600, 140
