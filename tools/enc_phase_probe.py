@@ -20,10 +20,12 @@ def sub(old, new):
 
 sub("  int pending = -1;  // item whose TMA this subgroup already issued\n",
     "  int pending = -1;  // item whose TMA this subgroup already issued\n"
-    "  unsigned long long ph_[10] = {0,0,0,0,0,0,0,0,0,0};\n"
+    "  unsigned long long ph_[12] = {0,0,0,0,0,0,0,0,0,0,0,0};\n"
     "  unsigned long long tprev_ = clock64(), nitems_ = 0;\n"
     "  auto mark_ = [&](int i) { const unsigned long long t = clock64(); ph_[i] += t - tprev_; tprev_ = t; };\n")
 sub("      mbar_wait(xfull, ph);\n", "      mark_(9);\n      mbar_wait(xfull, ph);\n      mark_(0);\n")
+sub("    if (u != staged) {\n      stage_patterns(A, SIDE, u, sb, gtid);\n      bar_side();\n      staged = u;\n    }\n",
+    "    mark_(10);\n    if (u != staged) {\n      stage_patterns(A, SIDE, u, sb, gtid);\n      bar_side();\n      staged = u;\n    }\n    mark_(11);\n")
 sub("      token_stage<SIDE>(sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats, u, start, L, c.bad);\n",
     "      token_stage<SIDE>(sc, pt, X, M, mmab, ph, tcol, w, lane, P, pmx, p64, stats, u, start, L, c.bad);\n"
     "      mark_(1);\n      ++nitems_;\n")
@@ -42,10 +44,10 @@ sub("      *cnext = (int)j0 + 4;\n    }\n    bar_side();\n  }\n}\n",
     "      *cnext = (int)j0 + 4;\n    }\n    bar_side();\n  }\n  mark_(9);\n"
     "  if (c.stats && blockIdx.x < 3 && lane == 0 && sgi < 2)\n"
     "    printf(\"ENC side %d cta %d warp %d items %llu | tma %.0f tok %.0f bar1 %.0f kpass %.0f bar2 %.0f scal %.0f "
-    "bar3 %.0f fix/codes %.0f next+store %.0f meta/chunk %.0f\\n\", SIDE, blockIdx.x, warp, nitems_,\n"
+    "bar3 %.0f fix/codes %.0f next+store %.0f meta %.0f chunkbar %.0f stage %.0f\\n\", SIDE, blockIdx.x, warp, nitems_,\n"
     "           ph_[0] / (double)nitems_, ph_[1] / (double)nitems_, ph_[2] / (double)nitems_, ph_[3] / (double)nitems_,\n"
     "           ph_[4] / (double)nitems_, ph_[5] / (double)nitems_, ph_[6] / (double)nitems_, ph_[7] / (double)nitems_,\n"
-    "           ph_[8] / (double)nitems_, ph_[9] / (double)nitems_);\n}\n")
+    "           ph_[8] / (double)nitems_, ph_[9] / (double)nitems_, ph_[10] / (double)nitems_, ph_[11] / (double)nitems_);\n}\n")
 os.makedirs(os.path.join(ROOT, "_ab"), exist_ok=True)
 open(os.path.join(ROOT, "_ab/enc_tc_t.cu"), "w").write(s)
 print(subprocess.run(["bash", os.path.join(ROOT, "tools/ab_build.sh"), "enc_tc_t", "pkv_encode_tc", "_ab/enc_tc_t.cu"],
