@@ -31,6 +31,16 @@ sub("      if (split) mbar_arrive_cnt(&empty[s], 2);  // this group alone consum
     "        atomicAdd(&g_mp[sd_][2], (r2_ - r1_) + (r4_ - r3_)); atomicAdd(&g_mp[sd_][5], 1ull);\n"
     "      }\n"
     "      if (split) mbar_arrive_cnt(&empty[s], 2);  // this group alone consumed the tile\n")
+# near-tie fp64 re-decision (row warps): cycles and entries
+sub("        if (__any_sync(0xffffffffu, tie)) {\n",
+    "        const unsigned long long t0_ = clock64();\n        const bool anyt_ = __any_sync(0xffffffffu, tie);\n"
+    "        if (anyt_) {\n")
+sub("          bi = bj;\n        }\n",
+    "          bi = bj;\n        }\n"
+    "        if (lane == 0 && (warp & 3) == 0) {\n"
+    "          const int sd_ = blockIdx.x >= gridDim.x / 2;\n"
+    "          atomicAdd(&g_mp[sd_][6], clock64() - t0_); atomicAdd(&g_mp[sd_][7], anyt_ ? 1ull : 0ull);\n"
+    "        }\n")
 # channel warps
 sub("        mbar_wait_sleep(&lready[ls], lph);\n",
     "        unsigned long long c0_ = clock64();\n        mbar_wait_sleep(&lready[ls], lph);\n        unsigned long long c1_ = clock64();\n")
@@ -46,8 +56,8 @@ sub("  if (warp == 1) tmem_free<256>(*sm.tmem);\n}",
     "  if (tid == 0) {\n    __threadfence();\n"
     "    if (atomicAdd(&g_mdone, 1u) == gridDim.x - 1) {\n"
     "      for (int sd = 0; sd < 2; ++sd) {\n        const double n = (double)g_mp[sd][5];\n"
-    "        if (n > 0) printf(\"MINE half %d tiles %.0f | row wait-tile %.0f wait-mma %.0f work %.0f | ch wait-labels %.0f sums %.0f (cycles/tile)\\n\",\n"
-    "               sd, n, g_mp[sd][0] / n, g_mp[sd][1] / n, g_mp[sd][2] / n, g_mp[sd][3] / n, g_mp[sd][4] / n);\n"
+    "        if (n > 0) printf(\"MINE half %d tiles %.0f | row wait-tile %.0f wait-mma %.0f work %.0f | ch wait-labels %.0f sums %.0f | ties %.0f cyc, %.3f of tiles (cycles/tile)\\n\",\n"
+    "               sd, n, g_mp[sd][0] / n, g_mp[sd][1] / n, g_mp[sd][2] / n, g_mp[sd][3] / n, g_mp[sd][4] / n, g_mp[sd][6] / n, g_mp[sd][7] / n);\n"
     "        for (int i = 0; i < 8; ++i) g_mp[sd][i] = 0;\n      }\n      g_mdone = 0;\n    }\n  }\n}")
 open(os.path.join(ROOT, "_ab/mine_t.cu"), "w").write(s)
 print(subprocess.run(["bash", os.path.join(ROOT, "tools/ab_build.sh"), "mine_t", "pkv_mine", "_ab/mine_t.cu"],
