@@ -59,7 +59,7 @@ def main():
     # gpurun_out/ by earlier captures would describe superseded kernels)
     pre = os.environ.get("PROF_PREFIX", "")  # e.g. "r2_" for tools/gpu_r2.sh captures
     reps = {n: os.path.join(OUT, pre + n + ".ncu-rep")
-            for n in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn")}
+            for n in ("prof_encode_full", "prof_attn_full", "prof_kmeans", "prof_encode", "prof_attn", "prof_merge")}
     newest = max((os.path.getmtime(r) for r in reps.values() if os.path.exists(r)), default=0.0)
     for name, rep in reps.items():
         if not os.path.exists(rep) or os.path.getmtime(rep) < newest - 3600:
@@ -73,7 +73,7 @@ def main():
         txt += "\n\nhot source lines (share of executed instructions / of stall samples):\n" + lines(rep)
         with open(os.path.join(PROF, f"{tag}_{name}.txt"), "w") as f:
             f.write(f"# ncu --set full capture: {name}.ncu-rep ({tag})\n\n" + txt)
-        if "dram__bytes_read.sum" in raw and "kmeans" not in name:
+        if "dram__bytes_read.sum" in raw and "kmeans" not in name and "merge" not in name:
             def to_bytes(v):
                 val, unit = float(v[0].replace(",", "")), v[1]
                 return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
