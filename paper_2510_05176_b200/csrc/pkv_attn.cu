@@ -545,115 +545,163 @@ __device__ __forceinline__ float to_f32<__half>(__half x) { return __half2float(
 template <>
 __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
 
-template <typename T, bool VEC, int GC>
+constexpr int MERGE_WT = 1024;  // window rows scored per tile (online softmax across tiles)
+
+template <typename T, bool VEC, int GC, bool TILED>
 __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_slot0, float* out) {
   extern __shared__ float msm[];
   constexpr int GM = GC > 0 ? GC : MAXG;  // compile-time head count (GC = 0: a.G at run time)
   const int u = blockIdx.x, G = GC > 0 ? GC : a.G, NTH = 32 * G;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int D = c.D, Dp = c.Dp, Wcap = c.Wcap;
+  // TILED: the window may exceed one score tile (else one tile: no rescale of the running sums)
+  const int D = c.D, Dp = c.Dp, Wcap = c.Wcap, WT = TILED ? MERGE_WT : Wcap;
   float* qs = msm;                 // [G][D] queries
-  float* sc = qs + G * D;          // [G][Wcap] scores, then probabilities
-  float* red = sc + G * Wcap;      // [G warps][G heads][D] partial outputs (VEC)
+  float* sc = qs + G * D;          // [G][WT] scores, then probabilities, of one window tile
+  float* rs = sc + G * WT;         // [G] per-head rescale of the running sums at this tile
+  float* red = msm + ((G * D + G * WT + G + 3) & ~3);  // [G warps][G heads][D] partial outputs (VEC), 16-B aligned
   for (int i = tid; i < G * D; i += NTH) qs[i] = a.q[(int64_t)u * G * D + i];
-  __syncthreads();
   const T* wk = reinterpret_cast<const T*>(c.wk) + (int64_t)u * Wcap * D;
   const T* wv = reinterpret_cast<const T*>(c.wv) + (int64_t)u * Wcap * D;
-  // (1) scores: thread per window row, all G heads
-  for (int r = tid; r < win_len; r += NTH) {
-    const int slot = win_slot0 + r;  // ring slot: win_slot0 < Wcap and r < Wcap
-    const T* kr = wk + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D;
-    float acc[GM];
+  const int h = w;                 // phase (2) / (4): warp h = head h
+  float m = -INFINITY, l = 0.f;    // head h's running max (log2 units) and sum
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc3[VEC ? GM : 1][4];     // VEC phase (3): this warp's rows, all heads
 #pragma unroll
-    for (int g = 0; g < GM; ++g) acc[g] = 0.f;
+  for (int g = 0; g < (VEC ? GM : 1); ++g)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc3[g][j] = 0.f;
+  auto tile = [&](int w0) {
+    const int wn = min(WT, win_len - w0);
+    __syncthreads();  // queries staged / the previous tile's probabilities consumed
+    // (1) scores: thread per window row, all G heads
+    for (int rr = tid; rr < wn; rr += NTH) {
+      const int slot = win_slot0 + w0 + rr;  // ring slot: win_slot0 < Wcap and w0 + rr < Wcap
+      const T* kr = wk + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D;
+      float acc[GM];
+#pragma unroll
+      for (int g = 0; g < GM; ++g) acc[g] = 0.f;
+      if constexpr (VEC) {
+        constexpr int NB = sizeof(T) == 8 ? 4 : 16;  // 4-element vectors in flight per batch
+        for (int d0 = 0; d0 < D; d0 += 4 * NB) {
+          typename Vec4<T>::raw kv[NB];
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            if (d0 + 4 * j < D) kv[j] = ld4(kr + d0 + 4 * j);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            if (d0 + 4 * j >= D) break;
+            const float4 k4 = cvt4(kv[j], (const T*)nullptr);
+#pragma unroll
+            for (int g = 0; g < GM; ++g) {
+              if (g >= G) break;
+              const float4 q4 = *reinterpret_cast<const float4*>(qs + g * D + d0 + 4 * j);
+              acc[g] = fmaf(q4.x, k4.x, fmaf(q4.y, k4.y, fmaf(q4.z, k4.z, fmaf(q4.w, k4.w, acc[g]))));
+            }
+          }
+        }
+      } else {
+#pragma unroll 4
+        for (int d = 0; d < D; ++d) {
+          const float kv = to_f32(kr[d]);
+#pragma unroll
+          for (int g = 0; g < GM; ++g)
+            if (g < G) acc[g] = fmaf(qs[g * D + d], kv, acc[g]);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < GM; ++g)
+        if (g < G) sc[g * WT + rr] = acc[g] * a.scale_log2;
+    }
+    __syncthreads();
+    // (2) warp h: tile max, running max, probabilities, running sum (log2 units)
+    {
+      float* sh = sc + h * WT;
+      float mt = -INFINITY;
+      for (int rr = lane; rr < wn; rr += 32) mt = fmaxf(mt, sh[rr]);
+#pragma unroll
+      for (int off = 16; off; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+      const float mn = fmaxf(m, mt);
+      const float al = m == -INFINITY ? 0.f : exp2f(m - mn);
+      float lt = 0.f;
+      for (int rr = lane; rr < wn; rr += 32) {
+        const float p = exp2f(sh[rr] - mn);
+        sh[rr] = p;
+        lt += p;
+      }
+      l = l * al + warp_sum_f(lt);
+      m = mn;
+      if (!TILED) {
+      } else if (VEC) {
+        if (lane == 0) rs[h] = al;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] *= al;
+      }
+    }
     if constexpr (VEC) {
-      constexpr int NB = 16;       // 4-element vectors in flight per batch
-      for (int d0 = 0; d0 < D; d0 += 4 * NB) {
-        typename Vec4<T>::raw kv[NB];
+      __syncthreads();
+      // (3) warp w: rows r = w (mod G) of the tile, all heads, lane = channels 4*lane .. 4*lane+3
 #pragma unroll
-        for (int j = 0; j < NB; ++j)
-          if (d0 + 4 * j < D) kv[j] = ld4(kr + d0 + 4 * j);
+      for (int g = 0; g < GM; ++g) {
+        if (g >= G || !TILED) break;
+        const float al = rs[g];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          if (d0 + 4 * j >= D) break;
-          const float4 k4 = cvt4(kv[j], (const T*)nullptr);
+        for (int j = 0; j < 4; ++j) acc3[g][j] *= al;
+      }
+      const bool on = 4 * lane < D;
+      constexpr int RB = 8;
+      for (int r0 = w; r0 < wn; r0 += RB * G) {
+        typename Vec4<T>::raw vv[RB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const int rr = r0 + i * G;
+          const int slot = win_slot0 + w0 + rr;
+          if (on && rr < wn) vv[i] = ld4(wv + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D + 4 * lane);
+        }
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const int rr = r0 + i * G;
+          if (rr >= wn) break;
+          const float4 v4 = on ? cvt4(vv[i], (const T*)nullptr) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int g = 0; g < GM; ++g) {
             if (g >= G) break;
-            const float4 q4 = *reinterpret_cast<const float4*>(qs + g * D + d0 + 4 * j);
-            acc[g] = fmaf(q4.x, k4.x, fmaf(q4.y, k4.y, fmaf(q4.z, k4.z, fmaf(q4.w, k4.w, acc[g]))));
+            const float p = sc[g * WT + rr];
+            acc3[g][0] = fmaf(p, v4.x, acc3[g][0]);
+            acc3[g][1] = fmaf(p, v4.y, acc3[g][1]);
+            acc3[g][2] = fmaf(p, v4.z, acc3[g][2]);
+            acc3[g][3] = fmaf(p, v4.w, acc3[g][3]);
           }
         }
       }
     } else {
-#pragma unroll 4
-      for (int d = 0; d < D; ++d) {
-        const float kv = to_f32(kr[d]);
+      __syncwarp();
+      // (3) o = sum_r p_r v_r for head h, lanes over channels
+      const float* sh = sc + h * WT;
+#pragma unroll 2
+      for (int rr = 0; rr < wn; ++rr) {
+        const int slot = win_slot0 + w0 + rr;
+        const T* vr = wv + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D;
+        const float p = sh[rr];
 #pragma unroll
-        for (int g = 0; g < GM; ++g)
-          if (g < G) acc[g] = fmaf(qs[g * D + d], kv, acc[g]);
+        for (int j = 0; j < 4; ++j)
+          if (lane + 32 * j < D) o[j] = fmaf(p, to_f32(vr[lane + 32 * j]), o[j]);
       }
     }
-#pragma unroll
-    for (int g = 0; g < GM; ++g)
-      if (g < G) sc[g * Wcap + r] = acc[g] * a.scale_log2;
+  };
+  if constexpr (TILED) {
+    for (int w0 = 0; w0 < win_len; w0 += WT) tile(w0);
+  } else {  // one tile: the running sums are born in phase (3), not carried across a loop
+    tile(0);
   }
-  __syncthreads();
-  // (2) warp h = w: running max, probabilities, sum (log2 units)
-  const int h = w;
-  float* sh = sc + h * Wcap;
-  float m = -INFINITY;
-  for (int r = lane; r < win_len; r += 32) m = fmaxf(m, sh[r]);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float l = 0.f;
-  for (int r = lane; r < win_len; r += 32) {
-    const float p = exp2f(sh[r] - m);
-    sh[r] = p;
-    l += p;
-  }
-  l = warp_sum_f(l);
-  float o[4] = {0.f, 0.f, 0.f, 0.f};
   if constexpr (VEC) {
-    __syncthreads();
-    // (3) warp w: rows r = w (mod G), all heads, lane = channels 4*lane .. 4*lane+3
-    float acc[GM][4];
-#pragma unroll
-    for (int g = 0; g < GM; ++g)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[g][j] = 0.f;
     const bool on = 4 * lane < D;
-    constexpr int RB = 8;
-    for (int r0 = w; r0 < win_len; r0 += RB * G) {
-      typename Vec4<T>::raw vv[RB];
-#pragma unroll
-      for (int i = 0; i < RB; ++i) {
-        const int r = r0 + i * G;
-        const int slot = win_slot0 + r;
-        if (on && r < win_len) vv[i] = ld4(wv + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D + 4 * lane);
-      }
-#pragma unroll
-      for (int i = 0; i < RB; ++i) {
-        const int r = r0 + i * G;
-        if (r >= win_len) break;
-        const float4 v4 = on ? cvt4(vv[i], (const T*)nullptr) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int g = 0; g < GM; ++g) {
-          if (g >= G) break;
-          const float p = sc[g * Wcap + r];
-          acc[g][0] = fmaf(p, v4.x, acc[g][0]);
-          acc[g][1] = fmaf(p, v4.y, acc[g][1]);
-          acc[g][2] = fmaf(p, v4.z, acc[g][2]);
-          acc[g][3] = fmaf(p, v4.w, acc[g][3]);
-        }
-      }
-    }
     if (on) {
 #pragma unroll
       for (int g = 0; g < GM; ++g)
         if (g < G)
           *reinterpret_cast<float4*>(red + ((int64_t)w * G + g) * D + 4 * lane) =
-              make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+              make_float4(acc3[g][0], acc3[g][1], acc3[g][2], acc3[g][3]);
     }
     __syncthreads();
     if (on)
@@ -661,18 +709,6 @@ __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_s
         const float4 x = *reinterpret_cast<const float4*>(red + ((int64_t)ww * G + h) * D + 4 * lane);
         o[0] += x.x; o[1] += x.y; o[2] += x.z; o[3] += x.w;
       }
-  } else {
-    __syncwarp();
-    // (3) o = sum_r p_r v_r for head h, lanes over channels
-#pragma unroll 2
-    for (int r = 0; r < win_len; ++r) {
-      const int slot = win_slot0 + r;
-      const T* vr = wv + (int64_t)(slot >= Wcap ? slot - Wcap : slot) * D;
-      const float p = sh[r];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (lane + 32 * j < D) o[j] = fmaf(p, to_f32(vr[lane + 32 * j]), o[j]);
-    }
   }
   // channel of o[j]: VEC 4*lane + j, else lane + 32*j
   auto chan = [&](int j) { return VEC ? 4 * lane + j : lane + 32 * j; };
@@ -704,12 +740,14 @@ __global__ void attn_merge_kernel(DevCache c, AttnArgs a, int win_len, int win_s
   for (int j = 0; j < 4; ++j) if (chan(j) < D) dst[chan(j)] = o[j] * inv;
 }
 
-template <typename T, bool VEC, int GC>
+template <typename T, bool VEC, int GC, bool TILED>
 static cudaError_t launch_merge(const DevCache& c, const AttnArgs& a, int win_len, int win_slot0, float* out,
                                 cudaStream_t st) {
-  const size_t msmem = ((size_t)a.G * c.D + (size_t)a.G * c.Wcap + (VEC ? (size_t)a.G * a.G * c.D : 0)) * 4;
+  const size_t msmem =
+      ((((size_t)a.G * c.D + (size_t)a.G * (TILED ? MERGE_WT : c.Wcap) + a.G + 3) & ~(size_t)3) +
+       (VEC ? (size_t)a.G * a.G * c.D : 0)) * 4;
   if (msmem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(attn_merge_kernel<T, VEC, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t e = cudaFuncSetAttribute(attn_merge_kernel<T, VEC, GC, TILED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)msmem);
     if (e != cudaSuccess) return e;
   }
@@ -726,16 +764,20 @@ static cudaError_t launch_merge(const DevCache& c, const AttnArgs& a, int win_le
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = a.nchunk > 0 ? 1 : 0;  // no chunk grid: the predecessor may be the window writer
-  return cudaLaunchKernelEx(&cfg, attn_merge_kernel<T, VEC, GC>, c, a, win_len, win_slot0, out);
+  return cudaLaunchKernelEx(&cfg, attn_merge_kernel<T, VEC, GC, TILED>, c, a, win_len, win_slot0, out);
 }
 
 template <typename T, bool VEC>
 static cudaError_t launch_merge_g(const DevCache& c, const AttnArgs& a, int win_len, int win_slot0, float* out,
                                   cudaStream_t st) {
+  const bool tiled = c.Wcap > MERGE_WT;  // score tile of every window row fits smem otherwise
   switch (a.G) {
-    case 4: return launch_merge<T, VEC, 4>(c, a, win_len, win_slot0, out, st);
-    case 8: return launch_merge<T, VEC, 8>(c, a, win_len, win_slot0, out, st);
-    default: return launch_merge<T, VEC, 0>(c, a, win_len, win_slot0, out, st);
+    case 4: return tiled ? launch_merge<T, VEC, 4, true>(c, a, win_len, win_slot0, out, st)
+                         : launch_merge<T, VEC, 4, false>(c, a, win_len, win_slot0, out, st);
+    case 8: return tiled ? launch_merge<T, VEC, 8, true>(c, a, win_len, win_slot0, out, st)
+                         : launch_merge<T, VEC, 8, false>(c, a, win_len, win_slot0, out, st);
+    default: return tiled ? launch_merge<T, VEC, 0, true>(c, a, win_len, win_slot0, out, st)
+                          : launch_merge<T, VEC, 0, false>(c, a, win_len, win_slot0, out, st);
   }
 }
 

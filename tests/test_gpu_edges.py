@@ -298,3 +298,24 @@ def test_fused_nonfinite_detection(pkv, dtype):
     cache.prefill(kt[:, :T], vt[:, :T], sync_check=True)
     for t in range(T, T + 4):
         cache.append(kt[:, t], vt[:, t], sync_check=True)
+
+
+@pytest.mark.parametrize("d,gqa,dt", [(128, 4, torch.float16), (42, 3, torch.float16), (64, 8, torch.float32)])
+def test_long_window_merge_tiles(pkv, d, gqa, dt):
+    """A residual window longer than the merge kernel's 1024-row score tile (online softmax across
+    window tiles, ring wrap after appends): attention within 1e-3 of fp64 softmax; vector-load
+    (d % 4 == 0) and scalar paths, compile-time and run-time head counts, fp16 and fp32 rows."""
+    from paper_2510_05176_b200.config import EngineConfig
+
+    U, T, S = 2, 2900, 300
+    ec = EngineConfig(bits=2, pattern_count=8, group_size=128, residual_window=1500)
+    k, v = _units(U, T + S, d, seed=7 + d)
+    cache = pkv.PatternKVCache(ec, U, d, dtype=dt, max_tokens=T + S + 256)
+    kt, vt = torch.from_numpy(k).to(dt).cuda(), torch.from_numpy(v).to(dt).cuda()
+    cache.prefill(kt[:, :T], vt[:, :T])
+    assert cache.info().window_len > 1024
+    _attention_close(pkv, cache, U, d, G=gqa)
+    for t in range(T, T + S):
+        cache.append(kt[:, t], vt[:, t])
+    assert cache.info().window_len > 1024 and cache.info().window_slot0 > 0
+    _attention_close(pkv, cache, U, d, G=gqa, seed=5)
