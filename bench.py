@@ -46,7 +46,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
-ALL_LEGS = ("decode_loop", "refgen", "cfg3", "cfg4", "cfg5_head")
+ALL_LEGS = ("decode_loop", "mining_full", "refgen", "cfg3", "cfg4", "cfg5_head")
 
 
 def hbm_peak():
@@ -342,6 +342,20 @@ def leg_encode(ctx, bits: int, k, v, pool_patterns, results, want_e2e: bool):
     # ---- end-to-end through the public API with host buffers -----------------------------
     if want_e2e:
         r["e2e"] = leg_e2e(ctx, cfgE, k, v, pk, pv, q, out, cache)
+
+    # ---- full prefill of every unit: mining (both sides, one launch) + encode -------------
+    # the `mining` key times the distinct pool only (256 units: 512 CTAs on 148 SMs, whose
+    # wave quantisation dominates); this is the per-GPU cfg2 prefill as a deployment runs it
+    if "mining_full" in args.legs and want_e2e:
+        cache.reset(keep_patterns=False)
+        cache.reserve_mining(T)
+        pre_ms, _ = ctx.time_steps(lambda: (cache.reset(keep_patterns=False), cache.prefill(k, v)), 1, 0,
+                                   clocks=False)
+        r["mining_full"] = {"units": U, "sides": 2, "prefill_ms": pre_ms, "encode_ms": kern_ms,
+                            "mining_ms": pre_ms - kern_ms,
+                            "note": "one timed prefill of all units from HBM (K2 mining of both sides in one "
+                                    "launch + K1-TC encode + window copy); mining_ms = prefill_ms - the encode "
+                                    "step's device time"}
     del cache
     torch.cuda.empty_cache()
     results[bits] = r
@@ -907,6 +921,7 @@ def main():
                         "e2e_h2d_bytes": e2e["attn_h2d"], "e2e_d2h_bytes": e2e["attn_d2h"],
                         "kernel": "attn_tc_kernel (K3-TC: tcgen05 kind::i8, integer code planes from TMEM) + attn_merge_kernel", "clocks": r["clk_a"],
                         "traffic": ncu_traffic("attn", U * committed)},
+        "mining_full": r.get("mining_full"),
         "mining": {"ms": r["mine_ms"], "units": pool, "sides": 2, "tokens": T, "patterns": args.patterns,
                    "scratch": "preallocated outside the timed region (PatternKVCache.reserve_mining)",
                    "kernel": "kmeans_stream_kernel: one TMA stream per pass, distance GEMM on tcgen05 (TMEM), exact fp64 "
