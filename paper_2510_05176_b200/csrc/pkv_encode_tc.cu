@@ -1107,8 +1107,9 @@ __device__ __forceinline__ void v_scalar(const Args& A, const unsigned char* X, 
     if (c.keep_diag && c.vdiag) { c.vdiag[2 * tok] = raw; c.vdiag[2 * tok + 1] = flat; }
   }
 }
-// codes pass of one 8-token row-set (rows rb + g): codes, exact fix-ups, movmatrix to the
-// V^T fragment layout, this row-set's words of the tile
+// codes pass of two 8-token row-sets (rows rb + g and rb + 8 + g, rb a multiple of 16): codes,
+// exact fix-ups, movmatrix to the V^T fragment layout, the two row-sets' interleaved words of
+// the tile in one 64-bit store each (two independent row-sets per call: twice the ILP of one)
 template <int BITS>
 __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, int blk_bytes, int64_t Tcap,
                                      const unsigned char* X, const float* M, Scr sc, int rb, int lane, int L, int u,
@@ -1119,71 +1120,85 @@ __device__ __noinline__ void v_codes(uint8_t* vcodes, const double* vparam64, in
   constexpr int HS = 8 / BITS;
   constexpr int WL = 128 * BITS / 64;
   const int g = lane >> 2, q = lane & 3;
-  const int t = rb + g, h = (rb >> 3) & 1;
-  const int idx = sc.fidx()[t];
-  const bool flatten = (sc.info()[t] >> 15) & 1;
-  const float lo32 = sc.lo32()[t], inv = sc.inv()[t], hg = sc.hg()[t];
-  float r[8][4];
-  float d0, d1, d2, d3;
-  resid_row(X, M, rb, lane, idx, r, d0, d1, d2, d3);
-  if (!flatten) {  // RAW payload: the exact input row (rare)
+  uint32_t pp[2][16];
+  uint32_t badm[2];
+  int idx[2];
+  bool flatten[2];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+  for (int n = 0; n < 2; ++n) {
+    const int t = rb + 8 * n + g;
+    idx[n] = sc.fidx()[t];
+    flatten[n] = (sc.info()[t] >> 15) & 1;
+    const float lo32 = sc.lo32()[t], inv = sc.inv()[t], hg = sc.hg()[t];
+    float r[8][4];
+    float d0, d1, d2, d3;
+    resid_row(X, M, rb + 8 * n, lane, idx[n], r, d0, d1, d2, d3);
+    if (!flatten[n]) {  // RAW payload: the exact input row (rare)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) r[j][e] = xt_at(X, t, 16 * j + 8 * (e >> 1) + 2 * q + (e & 1));
-  }
-  uint32_t pp[16];
-  uint32_t badm = 0;
-  const float2 nlo2 = make_float2(-lo32, -lo32), inv2 = make_float2(inv, inv);
+      for (int j = 0; j < 8; ++j)
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    bool bad0 = false, bad1 = false;
-    const float2 z01 = zcode2s(make_float2(r[j][0], r[j][1]), nlo2, inv2, hg, bad0);
-    const float2 z23 = zcode2s(make_float2(r[j][2], r[j][3]), nlo2, inv2, hg, bad1);
-    pp[2 * j] = zpair(z01.x, z01.y);
-    pp[2 * j + 1] = zpair(z23.x, z23.y);
-    badm |= ((uint32_t)bad0 << (2 * j)) | ((uint32_t)bad1 << (2 * j + 1));
-  }
-  if (t >= L) {
-    badm = 0;
+        for (int e = 0; e < 4; ++e) r[j][e] = xt_at(X, t, 16 * j + 8 * (e >> 1) + 2 * q + (e & 1));
+    }
+    badm[n] = 0;
+    const float2 nlo2 = make_float2(-lo32, -lo32), inv2 = make_float2(inv, inv);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) pp[i] = 0u;
-  }
-  if (badm) {  // rare: the reference's fp64 sequence decides inside the guard band (deferred to
-               // kfix_kernel through the fix list; in line when the list is full)
-    const double* mr = flatten ? p64 + (int64_t)idx * 128 : nullptr;
-    const __half* xrow = xsrc + (int64_t)t * 128;
-    const double* vp = vparam64 + 2 * ((int64_t)u * Tcap + start + t);
-#pragma unroll 1
-    while (badm) {
-      const int i = __ffs(badm) - 1;
-      badm &= badm - 1;
-      const int ca = 16 * (i >> 1) + 8 * (i & 1) + 2 * q;
-      const int fs = fix ? atomicAdd(fixcnt, 1) : fixcap;
-      if (fs < fixcap) {  // V entry: block, token, first channel of the pair, side bit 63
-        fix[fs] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ca << 39) |
-                  (1ull << 63);
-        continue;
-      }
-      const uint32_t pv = exact_code_p(xrow + ca, mr ? mr + ca : nullptr, vp + 1, vp, QMAX) |
-                          (exact_code_p(xrow + ca + 1, mr ? mr + ca + 1 : nullptr, vp + 1, vp, QMAX) << 16);
+    for (int j = 0; j < 8; ++j) {
+      bool bad0 = false, bad1 = false;
+      const float2 z01 = zcode2s(make_float2(r[j][0], r[j][1]), nlo2, inv2, hg, bad0);
+      const float2 z23 = zcode2s(make_float2(r[j][2], r[j][3]), nlo2, inv2, hg, bad1);
+      pp[n][2 * j] = zpair(z01.x, z01.y);
+      pp[n][2 * j + 1] = zpair(z23.x, z23.y);
+      badm[n] |= ((uint32_t)bad0 << (2 * j)) | ((uint32_t)bad1 << (2 * j + 1));
+    }
+    if (t >= L) {
+      badm[n] = 0;
 #pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) pp[k2] = k2 == i ? pv : pp[k2];
-      if (stats) atomicAdd(&stats[1], 1u);
+      for (int i = 0; i < 16; ++i) pp[n][i] = 0u;
     }
   }
-  uint32_t words[WL / 2];
 #pragma unroll
-  for (int i = 0; i < WL / 2; ++i) words[i] = 0u;
+  for (int n = 0; n < 2; ++n) {
+    if (badm[n]) {  // rare: the reference's fp64 sequence decides inside the guard band (deferred
+                    // to kfix_kernel through the fix list; in line when the list is full)
+      const int t = rb + 8 * n + g;
+      const double* mr = flatten[n] ? p64 + (int64_t)idx[n] * 128 : nullptr;
+      const __half* xrow = xsrc + (int64_t)t * 128;
+      const double* vp = vparam64 + 2 * ((int64_t)u * Tcap + start + t);
+      uint32_t bm = badm[n];
+#pragma unroll 1
+      while (bm) {
+        const int i = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const int ca = 16 * (i >> 1) + 8 * (i & 1) + 2 * q;
+        const int fs = fix ? atomicAdd(fixcnt, 1) : fixcap;
+        if (fs < fixcap) {  // V entry: block, token, first channel of the pair, side bit 63
+          fix[fs] = (unsigned long long)(uint32_t)blk | ((unsigned long long)t << 32) | ((unsigned long long)ca << 39) |
+                    (1ull << 63);
+          continue;
+        }
+        const uint32_t pv = exact_code_p(xrow + ca, mr ? mr + ca : nullptr, vp + 1, vp, QMAX) |
+                            (exact_code_p(xrow + ca + 1, mr ? mr + ca + 1 : nullptr, vp + 1, vp, QMAX) << 16);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t t0v = movm_t(pp[2 * j]), t1v = movm_t(pp[2 * j + 1]);  // hiRow 0 / 1 of sub-tile j
-    const int s0 = 2 * (j % HS);
-    words[j / HS] |= (t0v << (s0 * BITS)) | (t1v << ((s0 + 1) * BITS));
+        for (int k2 = 0; k2 < 16; ++k2) pp[n][k2] = k2 == i ? pv : pp[n][k2];
+        if (stats) atomicAdd(&stats[1], 1u);
+      }
+    }
   }
-  uint32_t* dst = reinterpret_cast<uint32_t*>(vcodes + blk * blk_bytes + (size_t)((rb >> 4) * 32 + lane) * WL * 4);
+  uint32_t words[2][WL / 2];
 #pragma unroll
-  for (int i = 0; i < WL / 2; ++i) dst[h + 2 * i] = words[i];
+  for (int n = 0; n < 2; ++n) {
+#pragma unroll
+    for (int i = 0; i < WL / 2; ++i) words[n][i] = 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t t0v = movm_t(pp[n][2 * j]), t1v = movm_t(pp[n][2 * j + 1]);  // hiRow 0 / 1 of sub-tile j
+      const int s0 = 2 * (j % HS);
+      words[n][j / HS] |= (t0v << (s0 * BITS)) | (t1v << ((s0 + 1) * BITS));
+    }
+  }
+  uint2* dst = reinterpret_cast<uint2*>(vcodes + blk * blk_bytes + (size_t)((rb >> 4) * 32 + lane) * WL * 4);
+#pragma unroll
+  for (int i = 0; i < WL / 2; ++i) dst[i] = make_uint2(words[0][i], words[1][i]);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1319,8 +1334,8 @@ __device__ __forceinline__ void run_sub(const Args& A, unsigned char* sb, const 
         v_scalar<BITS>(A, X, M, pt, sc, st, L, start, u, blk, p64, stats);
         __syncwarp();
 #pragma unroll 1
-        for (int rs = 0; rs < 4; ++rs)
-          v_codes<BITS>(c.vcodes, c.vparam64, c.blk_bytes, c.Tcap, X, M, sc, 32 * w + 8 * rs, lane, L, u, start, blk, xsrc,
+        for (int rs = 0; rs < 2; ++rs)
+          v_codes<BITS>(c.vcodes, c.vparam64, c.blk_bytes, c.Tcap, X, M, sc, 32 * w + 16 * rs, lane, L, u, start, blk, xsrc,
                         p64, stats, c.fix, c.fixcap, c.work + 2);
       }
       // release the x tile; the last warp out takes the subgroup's next item (this chunk's
