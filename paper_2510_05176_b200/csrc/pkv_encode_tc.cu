@@ -160,6 +160,24 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
 }
 __device__ __forceinline__ float h2f_lo(uint32_t v) { return __half2float(__ushort_as_half((unsigned short)(v & 0xffffu))); }
 __device__ __forceinline__ float h2f_hi(uint32_t v) { return __half2float(__ushort_as_half((unsigned short)(v >> 16))); }
+// x - m for an fp16 x (low / high half of v) and an fp32 m in ONE instruction (FHADD: the
+// mixed-precision sub.rn.f32.f16 converts x exactly and rounds once -- the same value as
+// converting and then subtracting, without the conversion instruction)
+__device__ __forceinline__ float subh_lo(uint32_t v, float m) {
+  float d;
+  asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(d) : "h"((unsigned short)(v & 0xffffu)), "f"(m));
+  return d;
+}
+__device__ __forceinline__ float subh_hi(uint32_t v, float m) {
+  float d;
+  asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(d) : "h"((unsigned short)(v >> 16)), "f"(m));
+  return d;
+}
+// running fp16 extrema of packed x (exact: max/min commute with the exact fp16 -> fp32
+// conversion; NaN lanes lose to numbers as in fmaxf), converted once at the end
+__device__ __forceinline__ __half2 u2h2(uint32_t v) { return *reinterpret_cast<const __half2*>(&v); }
+__device__ __forceinline__ float h2max(__half2 h) { return fmaxf(__low2float(h), __high2float(h)); }
+__device__ __forceinline__ float h2min(__half2 h) { return fminf(__low2float(h), __high2float(h)); }
 // value with its low mantissa bits replaced by an element index
 __device__ __forceinline__ float fkey(float v, uint32_t idx, uint32_t mask) {
   return __uint_as_float((__float_as_uint(v) & mask) | idx);
@@ -392,9 +410,11 @@ __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* 
   const float* m0p = M + idx[0] * 128 + q * 32;
   const float* m1p = M + idx[1] * 128 + q * 32;
   const int sw0 = (2 * q) ^ (idx[0] & 1), sw1 = (2 * q) ^ (idx[1] & 1);
+  __half2 hx[2], hn[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    st.kmx[h] = -FE_INF; st.kmn[h] = FE_INF; st.xmx[h] = -FE_INF; st.xmn[h] = FE_INF;
+    st.kmx[h] = -FE_INF; st.kmn[h] = FE_INF;
+    hx[h] = u2h2(0xfc00fc00u); hn[h] = u2h2(0x7c007c00u);  // -inf / +inf
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -403,16 +423,12 @@ __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* 
     ldsm_x4(addr, a0, a1, a2, a3);
     const float4 m0 = *reinterpret_cast<const float4*>(m0p + 4 * (j ^ sw0));
     const float4 m1 = *reinterpret_cast<const float4*>(m1p + 4 * (j ^ sw1));
-    const float x0[4] = {h2f_lo(a0), h2f_hi(a0), h2f_lo(a2), h2f_hi(a2)};
-    const float x1[4] = {h2f_lo(a1), h2f_hi(a1), h2f_lo(a3), h2f_hi(a3)};
-    const float2 ra = __fadd2_rn(make_float2(x0[0], x0[1]), make_float2(-m0.x, -m0.y));
-    const float2 rb = __fadd2_rn(make_float2(x0[2], x0[3]), make_float2(-m0.z, -m0.w));
-    const float2 rc = __fadd2_rn(make_float2(x1[0], x1[1]), make_float2(-m1.x, -m1.y));
-    const float2 rd = __fadd2_rn(make_float2(x1[2], x1[3]), make_float2(-m1.z, -m1.w));
-    const float rv[2][4] = {{ra.x, ra.y, rb.x, rb.y}, {rc.x, rc.y, rd.x, rd.y}};
+    const float rv[2][4] = {{subh_lo(a0, m0.x), subh_hi(a0, m0.y), subh_lo(a2, m0.z), subh_hi(a2, m0.w)},
+                            {subh_lo(a1, m1.x), subh_hi(a1, m1.y), subh_lo(a3, m1.z), subh_hi(a3, m1.w)}};
+    hx[0] = __hmax2(hx[0], __hmax2(u2h2(a0), u2h2(a2))); hn[0] = __hmin2(hn[0], __hmin2(u2h2(a0), u2h2(a2)));
+    hx[1] = __hmax2(hx[1], __hmax2(u2h2(a1), u2h2(a3))); hn[1] = __hmin2(hn[1], __hmin2(u2h2(a1), u2h2(a3)));
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const float* xx = h ? x1 : x0;
       const float k0 = KEYED ? fkey(rv[h][0], 4 * j + 0, 0xffffffe0u) : rv[h][0];
       const float k1 = KEYED ? fkey(rv[h][1], 4 * j + 1, 0xffffffe0u) : rv[h][1];
       const float k2 = KEYED ? fkey(rv[h][2], 4 * j + 2, 0xffffffe0u) : rv[h][2];
@@ -422,10 +438,10 @@ __device__ __forceinline__ void resid_tile(const unsigned char* X, const float* 
       }
       st.kmx[h] = fmax3(st.kmx[h], k0, k1); st.kmx[h] = fmax3(st.kmx[h], k2, k3);
       st.kmn[h] = fmin3(st.kmn[h], k0, k1); st.kmn[h] = fmin3(st.kmn[h], k2, k3);
-      st.xmx[h] = fmax3(st.xmx[h], xx[0], xx[1]); st.xmx[h] = fmax3(st.xmx[h], xx[2], xx[3]);
-      st.xmn[h] = fmin3(st.xmn[h], xx[0], xx[1]); st.xmn[h] = fmin3(st.xmn[h], xx[2], xx[3]);
     }
   }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) { st.xmx[h] = h2max(hx[h]); st.xmn[h] = h2min(hn[h]); }
 }
 
 __device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& a0, uint32_t& a1) {
@@ -442,23 +458,21 @@ __device__ __forceinline__ void resid_row(const unsigned char* X, const float* M
   const int lchk = (lane >> 3) & 1;
   const float* mp = M + p * 128 + q * 32;
   const int sw = (2 * q) ^ (p & 1);
-  kmx = -FE_INF; kmn = FE_INF; xmx = -FE_INF; xmn = FE_INF;
+  kmx = -FE_INF; kmn = FE_INF;
+  __half2 hx = u2h2(0xfc00fc00u), hn = u2h2(0x7c007c00u);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     uint32_t a0, a1;
     ldsm_x2(xbase + (j >> 2) * 16384 + lrow * 128 + ((((2 * (j & 3) + lchk) ^ (lrow & 7))) << 4), a0, a1);
     const float4 m = *reinterpret_cast<const float4*>(mp + 4 * (j ^ sw));
-    const float x[4] = {h2f_lo(a0), h2f_hi(a0), h2f_lo(a1), h2f_hi(a1)};
-    const float2 ra = __fadd2_rn(make_float2(x[0], x[1]), make_float2(-m.x, -m.y));
-    const float2 rb = __fadd2_rn(make_float2(x[2], x[3]), make_float2(-m.z, -m.w));
-    r[j][0] = ra.x; r[j][1] = ra.y; r[j][2] = rb.x; r[j][3] = rb.y;
+    r[j][0] = subh_lo(a0, m.x); r[j][1] = subh_hi(a0, m.y); r[j][2] = subh_lo(a1, m.z); r[j][3] = subh_hi(a1, m.w);
+    hx = __hmax2(hx, __hmax2(u2h2(a0), u2h2(a1))); hn = __hmin2(hn, __hmin2(u2h2(a0), u2h2(a1)));
     const float k0 = fkey(r[j][0], 4 * j + 0, 0xffffffe0u), k1 = fkey(r[j][1], 4 * j + 1, 0xffffffe0u);
     const float k2 = fkey(r[j][2], 4 * j + 2, 0xffffffe0u), k3 = fkey(r[j][3], 4 * j + 3, 0xffffffe0u);
     kmx = fmax3(kmx, k0, k1); kmx = fmax3(kmx, k2, k3);
     kmn = fmin3(kmn, k0, k1); kmn = fmin3(kmn, k2, k3);
-    xmx = fmax3(xmx, x[0], x[1]); xmx = fmax3(xmx, x[2], x[3]);
-    xmn = fmin3(xmn, x[0], x[1]); xmn = fmin3(xmn, x[2], x[3]);
   }
+  xmx = h2max(hx); xmn = h2min(hn);
 }
 __device__ __forceinline__ float qmax4(float v) {
   v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
@@ -786,9 +800,7 @@ __device__ __forceinline__ void k_load(const unsigned char* X, const float* M, c
     const uint32_t xb = *reinterpret_cast<const uint32_t*>(rowp + (((ck + 1) ^ (t & 7)) << 4));
     // mslot(p, q, jb) = q*32 + 4 ((jb ^ 2q) & 7) + (+-4 (p & 1), folded into fi[e])
     const float4 m = *reinterpret_cast<const float4*>(M + fi[e] + q * 32 + 4 * ((jb ^ (2 * q)) & 7));
-    const float2 ra = __fadd2_rn(make_float2(h2f_lo(xa), h2f_hi(xa)), make_float2(-m.x, -m.y));
-    const float2 rb = __fadd2_rn(make_float2(h2f_lo(xb), h2f_hi(xb)), make_float2(-m.z, -m.w));
-    rr[e][0] = ra.x; rr[e][1] = ra.y; rr[e][2] = rb.x; rr[e][3] = rb.y;
+    rr[e][0] = subh_lo(xa, m.x); rr[e][1] = subh_hi(xa, m.y); rr[e][2] = subh_lo(xb, m.z); rr[e][3] = subh_hi(xb, m.w);
     if (!FULL && t >= L) rr[e][0] = rr[e][1] = rr[e][2] = rr[e][3] = FE_NAN;
   }
 }
