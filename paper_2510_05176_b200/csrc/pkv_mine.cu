@@ -776,14 +776,16 @@ __device__ __forceinline__ float sk_d2_f32(uint32_t tile_s, int row, uint32_t s3
 #pragma unroll 4
   for (int q = 0; q < 16; ++q) {
     const uint4 v = lds128(sk_chunk(tile_s, row, q));
-    const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+    const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
     const uint4 sa = lds128(s32_s + 32 * q), sb = lds128(s32_s + 32 * q + 16);
     const float sv[8] = {__uint_as_float(sa.x), __uint_as_float(sa.y), __uint_as_float(sa.z), __uint_as_float(sa.w),
                          __uint_as_float(sb.x), __uint_as_float(sb.y), __uint_as_float(sb.z), __uint_as_float(sb.w)};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 f = __half22float2(h2[e]);
-      const float d0 = f.x - sv[2 * e], d1 = f.y - sv[2 * e + 1];
+      // x - s straight from the packed fp16 (one FHADD each: exact conversion, one rounding)
+      float d0, d1;
+      asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(d0) : "h"((unsigned short)(vw[e] & 0xffffu)), "f"(sv[2 * e]));
+      asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(d1) : "h"((unsigned short)(vw[e] >> 16)), "f"(sv[2 * e + 1]));
       a[e] = fmaf(d0, d0, a[e]);
       a[e] = fmaf(d1, d1, a[e]);
     }
@@ -1033,11 +1035,11 @@ __device__ void sk_pass(int mode, int64_t Tn, int k, const SkSmem& sm, const CUt
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch) {
             const uint4 w = lds128(sk_chunk(tile_s, row, 8 * half + ch));
-            const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __half22float2(h2[e]);
-              xq[e] = fmaf(f.x, f.x, fmaf(f.y, f.y, xq[e]));
+            for (int e = 0; e < 4; ++e) {  // x^2 + acc straight from fp16 (FHFMA, no conversion)
+              asm("fma.rn.f32.f16 %0, %1, %1, %0;" : "+f"(xq[e]) : "h"((unsigned short)(ww[e] >> 16)));
+              asm("fma.rn.f32.f16 %0, %1, %1, %0;" : "+f"(xq[e]) : "h"((unsigned short)(ww[e] & 0xffffu)));
             }
           }
         }
