@@ -923,6 +923,7 @@ def main():
                         "traffic": ncu_traffic("attn", U * committed)},
         "mining_full": r.get("mining_full"),
         "mining": {"ms": r["mine_ms"], "units": pool, "sides": 2, "tokens": T, "patterns": args.patterns,
+                   "ncu": _traffic_doc().get("kmeans") if _traffic_doc() else None,
                    "scratch": "preallocated outside the timed region (PatternKVCache.reserve_mining)",
                    "kernel": "kmeans_stream_kernel: one TMA stream per pass, distance GEMM on tcgen05 (TMEM), exact fp64 "
                              "centroid sums, objective from the sums in double-double"},

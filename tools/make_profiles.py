@@ -53,6 +53,7 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     traffic = {}
     instr = {}
+    kmeans_util = None
     # token-units (units x committed tokens) of the captured launches (tools/gpu_profiles.sh MED config)
     units = int(os.environ.get("PROF_UNITS", 2 * 32 * 8)) * int(os.environ.get("PROF_COMMITTED", 32768 - 128))
     # only reports from this capture: within an hour of the newest one (older reports left in
@@ -73,6 +74,18 @@ def main():
         txt += "\n\nhot source lines (share of executed instructions / of stall samples):\n" + lines(rep)
         with open(os.path.join(PROF, f"{tag}_{name}.txt"), "w") as f:
             f.write(f"# ncu --set full capture: {name}.ncu-rep ({tag})\n\n" + txt)
+        if "kmeans" in name:  # K2 utilisation for the bench line's `mining.ncu`
+            import re
+
+            def grab(label):
+                m = re.search(r"^" + re.escape(label) + r"\s+([0-9.,]+)", txt, re.M)
+                return float(m.group(1).replace(",", "")) if m else None
+            kmeans_util = {"dram_throughput_pct": grab("DRAM Throughput"), "l2_hit_pct": grab("L2 Hit Rate"),
+                           "issue_slots_busy_pct": grab("Issue Slots Busy"),
+                           "tensor_pipe_pct": grab("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                           "grid": grab("Grid Size"),
+                           "source": f"ncu --set full, {name}.ncu-rep ({tag}): one full K2 launch "
+                                     "(32 units x 2 sides = 64 CTAs, so device-wide % understate a full grid)"}
         if "dram__bytes_read.sum" in raw and "kmeans" not in name and "merge" not in name:
             def to_bytes(v):
                 val, unit = float(v[0].replace(",", "")), v[1]
@@ -87,7 +100,8 @@ def main():
             json.dump({"source": f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum ({tag}), "
                                  f"per token-unit of the captured launch ({units} token-units)",
                        "bytes_per_token_unit": traffic,
-                       "warp_instr_per_token_unit": instr}, f, indent=1)
+                       "warp_instr_per_token_unit": instr,
+                       "kmeans": kmeans_util}, f, indent=1)
     lp = os.path.join(OUT, pre + "launches.csv")
     if os.path.exists(lp):
         with open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w") as f:
